@@ -1,0 +1,53 @@
+// tcgen05/TMEM bf16 GEMM for the prefill projections (QKV, O, gate/up, down,
+// LM head). Swap-AB orientation: the WEIGHT matrix W[M=out_features, K] is the
+// MMA "A" operand (M = 128 rows per tile) and the token activations X[T, K]
+// are the "B" operand (N = tokens per tile, 16..256). So
+//     D[m, n] = sum_k W[m, k] * X[n, k]        (Y^T = W X^T)
+// Both operands are K-major, staged by TMA with 128-byte swizzle; the fp32
+// accumulator lives in TMEM (double-buffered so the epilogue of tile i
+// overlaps the mainloop of tile i+1). Persistent grid: one CTA per SM walks
+// (split, m_tile, n_tile) work units.
+//
+// For the short-prefill regime (T <= 256 tokens) the kernel is a weight
+// streamer: HBM-bound at T*... flop/byte well under the ridge; split-K keeps
+// all 148 SMs pulling weights when M/128 is small (O, down, QKV projections).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace lp {
+
+enum GemmEpilogue : int {
+  kEpiBf16 = 0,        // out_bf16[n*ldo + m] = acc (+ bias[m])
+  kEpiF32Partial = 1,  // ws[(split*ws_stride + n)*M + m] = acc
+  kEpiSiluMul = 2,     // rows interleaved (gate,up): out_bf16[n*ldo + m/2] = silu(g)*u
+  kEpiF32 = 3,         // out_f32[n*ldo + m] = acc
+};
+
+struct GemmArgs {
+  int M = 0;            // weight rows (output features)
+  int N = 0;            // token capacity (rows of X)
+  int K = 0;            // reduction length (multiple of 64)
+  int splits = 1;       // split-K factor
+  const int* n_dev = nullptr;  // optional device-side live token count (<= N)
+  int mode = kEpiBf16;
+  void* out = nullptr;
+  int ldo = 0;
+  const void* bias = nullptr;  // bf16[M] (kEpiBf16 only)
+  float* ws = nullptr;
+  int ws_stride = 0;    // rows per split slice in ws (>= N)
+};
+
+// Build a 2D bf16 tensor map over a row-major [rows, cols] matrix, box
+// [box_rows, 64 cols], 128-byte swizzle.
+CUtensorMap make_tmap_bf16(const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+
+// Launch. `bn` is the token-tile width (16, 32, 64, 128 or 256); tmB must have
+// been built with box_rows == bn.
+void gemm_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, int bn,
+                 cudaStream_t stream, int max_ctas = 0);
+
+int num_sms();
+
+}  // namespace lp

@@ -1,0 +1,89 @@
+"""tcgen05 GEMM parity vs a torch fp32 reference of the same op (bf16 inputs,
+fp32 accumulate). Tolerance: relative Frobenius error < 2e-3 and max-abs
+within bf16 output rounding."""
+import ctypes
+
+import pytest
+import torch
+
+from paper_2601_11589_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def run_gemm(M, Ntok, K, splits=1, mode=0, bn=None, bias=False, n_live=None, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    W = (torch.randn(M, K, device="cuda", generator=g) * 0.05).bfloat16()
+    X = torch.randn(Ntok, K, device="cuda", generator=g).bfloat16()
+    b = (torch.randn(M, device="cuda", generator=g) * 0.1).bfloat16() if bias else None
+    bn = bn or next(b for b in (16, 32, 64, 128, 256) if b >= min(Ntok, 256))
+    ref = X.float() @ W.float().t()  # [N, M]
+    if b is not None:
+        ref = ref + b.float()
+    nd = None
+    if n_live is not None:
+        nd = torch.tensor([n_live], dtype=torch.int32, device="cuda")
+    ws = None
+    if mode == 1:
+        ws = torch.zeros(splits, Ntok, M, device="cuda", dtype=torch.float32)
+        out = None
+        ldo = M
+    elif mode == 2:
+        out = torch.zeros(Ntok, M // 2, device="cuda", dtype=torch.bfloat16)
+        ldo = M // 2
+    elif mode == 3:
+        out = torch.zeros(Ntok, M, device="cuda", dtype=torch.float32)
+        ldo = M
+    else:
+        out = torch.zeros(Ntok, M, device="cuda", dtype=torch.bfloat16)
+        ldo = M
+    rc = N.lib().lpk_gemm(_ptr(W), _ptr(X), _ptr(out) if out is not None else None,
+                          _ptr(ws) if ws is not None else None, _ptr(b) if b is not None else None,
+                          M, Ntok, K, splits, mode, bn, ldo, _ptr(nd) if nd is not None else None, None)
+    N.check(rc)
+    torch.cuda.synchronize()
+    if mode == 1:
+        got = ws.sum(0)
+    elif mode == 2:
+        g_ = ref[:, 0::2].bfloat16().float()
+        u_ = ref[:, 1::2].bfloat16().float()
+        ref = torch.nn.functional.silu(g_) * u_
+        got = out.float()
+    else:
+        got = out.float()
+    return got, ref
+
+
+def _close(got, ref, n_live=None):
+    if n_live is not None:
+        got, ref = got[:n_live], ref[:n_live]
+    rel = (got - ref).norm() / ref.norm().clamp_min(1e-6)
+    assert rel < 5e-3, f"rel err {rel}"
+
+
+@pytest.mark.parametrize("M,Ntok,K", [(128, 16, 64), (256, 8, 512), (384, 100, 1024), (1024, 256, 3584),
+                                      (512, 600, 512), (4608, 64, 3584)])
+def test_gemm_bf16(M, Ntok, K):
+    got, ref = run_gemm(M, Ntok, K, bias=True)
+    _close(got, ref)
+
+
+@pytest.mark.parametrize("splits", [2, 5])
+def test_gemm_splitk(splits):
+    got, ref = run_gemm(3584, 200, 3584, splits=splits, mode=1)
+    _close(got, ref)
+
+
+def test_gemm_silu_mul():
+    got, ref = run_gemm(1536, 40, 256, mode=2)
+    _close(got, ref)
+
+
+def test_gemm_f32_and_live_count():
+    got, ref = run_gemm(1024, 256, 512, mode=3, n_live=77)
+    _close(got, ref, n_live=77)
+    assert torch.all(got[80:] == 0)
