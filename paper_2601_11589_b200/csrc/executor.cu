@@ -1,0 +1,594 @@
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <tuple>
+
+#include "abi_common.h"
+#include "executor.h"
+
+namespace lp {
+
+namespace {
+
+constexpr int kPage = kAttnPage;  // 64 tokens per KV page (== attention key tile)
+
+// Tensor ids for the counter-based weight generator (oracle/forward_oracle.py
+// uses the same numbering).
+constexpr uint64_t kTidEmbed = 1, kTidLmHead = 2;
+constexpr uint64_t kTidLayerBase = 1000, kTidLayerStride = 16;
+enum : uint64_t { kQkv = 0, kQkvBias = 1, kO = 2, kGate = 3, kUp = 4, kDown = 5 };
+
+template <typename T>
+T* dmalloc(size_t n, std::vector<void*>& owned) {
+  void* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+  if (e != cudaSuccess) {
+    throw OutOfMemory("cudaMalloc " + std::to_string(n * sizeof(T)) + " bytes: " +
+                      cudaGetErrorString(e));
+  }
+  owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+int pow2_bn(int t) {
+  int b = 16;
+  while (b < t && b < 256) b <<= 1;
+  return b;
+}
+
+int pick_splits(int m_tiles, int n_tiles, int num_kb, int sms) {
+  const int units = m_tiles * n_tiles;
+  if (units >= sms) return 1;
+  int s = sms / units;
+  s = std::min(s, std::max(1, num_kb / 4));
+  return std::max(1, std::min(s, 8));
+}
+
+}  // namespace
+
+Instance::Instance(const lp_model_desc& m, const lp_instance_desc& d) : m_(m), d_(d) {
+  if (m.head_dim != 64 && m.head_dim != 128) throw ConfigError("head_dim must be 64 or 128");
+  if (m.n_q_heads % m.n_kv_heads != 0) throw ConfigError("n_q_heads % n_kv_heads != 0");
+  if (m.hidden % 128 || ((m.n_q_heads + 2 * m.n_kv_heads) * m.head_dim) % 128 ||
+      (2 * m.intermediate) % 128 || m.vocab % 128 || m.intermediate % 64)
+    throw ConfigError("model dims must be multiples of 128 (hidden, qkv, 2*intermediate, vocab)");
+  if (d.page_size != 0 && d.page_size != kPage) throw ConfigError("page_size must be 64");
+  d_.page_size = kPage;
+  if (d_.max_tokens <= 0) d_.max_tokens = 16384;
+  if (d_.max_members <= 0) d_.max_members = 64;
+  lp_check(cudaSetDevice(d.device), "cudaSetDevice");
+  lp_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  lp_check(cudaEventCreate(&ev_start_), "event");
+  lp_check(cudaEventCreate(&ev_end_), "event");
+  alloc_weights();
+  alloc_arena();
+}
+
+Instance::~Instance() {
+  cudaSetDevice(d_.device);
+  cudaStreamSynchronize(stream_);
+  for (auto& [k, g] : graphs_) cudaGraphExecDestroy(g);
+  for (void* p : allocs_) cudaFree(p);
+  if (meta_host_) cudaFreeHost(meta_host_);
+  cudaEventDestroy(ev_start_);
+  cudaEventDestroy(ev_end_);
+  cudaStreamDestroy(stream_);
+}
+
+void Instance::alloc_weights() {
+  const int h = m_.hidden, I = m_.intermediate, D = m_.head_dim;
+  const int qkv_out = (m_.n_q_heads + 2 * m_.n_kv_heads) * D;
+  const int o_in = m_.n_q_heads * D;
+  const float scale = m_.init_std * std::sqrt(3.0f) / 8388608.0f;  // U(-a,a), a = std*sqrt(3)
+  const uint64_t seed = m_.weight_seed;
+  cudaStream_t st = stream_;
+  layers_.resize(m_.layers);
+  for (int l = 0; l < m_.layers; ++l) {
+    LayerW& w = layers_[l];
+    const uint64_t base = kTidLayerBase + kTidLayerStride * l;
+    w.wqkv = dmalloc<bf16>(size_t(qkv_out) * h, allocs_);
+    w.bqkv = dmalloc<bf16>(qkv_out, allocs_);
+    w.wo = dmalloc<bf16>(size_t(h) * o_in, allocs_);
+    w.wgu = dmalloc<bf16>(size_t(2) * I * h, allocs_);
+    w.wd = dmalloc<bf16>(size_t(h) * I, allocs_);
+    w.g_attn = dmalloc<bf16>(h, allocs_);
+    w.g_mlp = dmalloc<bf16>(h, allocs_);
+    init_weights(w.wqkv, size_t(qkv_out) * h, seed, base + kQkv, scale, 0, h, st);
+    init_weights(w.bqkv, qkv_out, seed, base + kQkvBias, scale, 0, 1, st);
+    init_weights(w.wo, size_t(h) * o_in, seed, base + kO, scale, 0, o_in, st);
+    init_weights(w.wgu, size_t(2) * I * h, seed, base + kGate, scale, /*interleave*/ 1, h, st);
+    init_weights(w.wd, size_t(h) * I, seed, base + kDown, scale, 0, I, st);
+    fill_bf16(w.g_attn, h, 1.0f, st);
+    fill_bf16(w.g_mlp, h, 1.0f, st);
+    w.tm_qkv = make_tmap_bf16(w.wqkv, qkv_out, h, 128);
+    w.tm_o = make_tmap_bf16(w.wo, h, o_in, 128);
+    w.tm_gu = make_tmap_bf16(w.wgu, 2 * I, h, 128);
+    w.tm_d = make_tmap_bf16(w.wd, h, I, 128);
+  }
+  embed_ = dmalloc<bf16>(size_t(m_.vocab) * h, allocs_);
+  lm_head_ = dmalloc<bf16>(size_t(m_.vocab) * h, allocs_);
+  g_final_ = dmalloc<bf16>(h, allocs_);
+  // Embedding rows ~ U(-sqrt3, sqrt3) (unit variance) so the residual stream
+  // starts O(1); every other tensor uses init_std.
+  init_weights(embed_, size_t(m_.vocab) * h, seed, kTidEmbed, std::sqrt(3.0f) / 8388608.0f, 0, h, st);
+  init_weights(lm_head_, size_t(m_.vocab) * h, seed, kTidLmHead, scale, 0, h, st);
+  fill_bf16(g_final_, h, 1.0f, st);
+  tm_lm_ = make_tmap_bf16(lm_head_, m_.vocab, h, 128);
+
+  std::vector<float> inv(D / 2);
+  for (int i = 0; i < D / 2; ++i)
+    inv[i] = static_cast<float>(1.0 / std::pow(static_cast<double>(m_.rope_theta), (2.0 * i) / D));
+  inv_freq_ = dmalloc<float>(D / 2, allocs_);
+  lp_check(cudaMemcpyAsync(inv_freq_, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice, st), "inv_freq");
+  lp_check(cudaGetLastError(), "weight init");
+  lp_check(cudaStreamSynchronize(st), "weight init sync");
+}
+
+void Instance::alloc_arena() {
+  const int h = m_.hidden, I = m_.intermediate, D = m_.head_dim;
+  const int qkv_out = (m_.n_q_heads + 2 * m_.n_kv_heads) * D;
+  const int G = m_.n_q_heads / m_.n_kv_heads;
+  t_max_ = static_cast<int>(d_.max_tokens);
+  r_max_ = d_.max_members;
+  w_max_ = (t_max_ * G + kAttnRows - 1) / kAttnRows + r_max_;
+
+  x_resid_ = dmalloc<float>(size_t(t_max_) * h, allocs_);
+  x_norm_ = dmalloc<bf16>(size_t(t_max_) * h, allocs_);
+  q_ = dmalloc<bf16>(size_t(t_max_) * m_.n_q_heads * D, allocs_);
+  attn_ = dmalloc<bf16>(size_t(t_max_) * m_.n_q_heads * D, allocs_);
+  act_ = dmalloc<bf16>(size_t(t_max_) * I, allocs_);
+  x_last_ = dmalloc<bf16>(size_t(std::max(r_max_, 256)) * h, allocs_);
+  logits_ = dmalloc<float>(size_t(r_max_) * m_.vocab, allocs_);
+  next_tok_ = dmalloc<int>(r_max_, allocs_);
+
+  // Split-K workspace: max over every capacity we may launch with.
+  ws_elems_ = 0;
+  for (int t = 16; t <= t_max_; t += 16) {
+    const SplitPlan p = plan_for(t, 1);
+    const size_t mx = std::max<size_t>({size_t(p.s_qkv) * qkv_out, size_t(p.s_o) * h,
+                                        size_t(p.s_d) * h});
+    ws_elems_ = std::max(ws_elems_, mx * size_t(t));
+  }
+  ws_ = dmalloc<float>(ws_elems_, allocs_);
+
+  // KV pool.
+  page_elems_ = size_t(2) * m_.n_kv_heads * kPage * D;
+  const size_t page_bytes_all = page_elems_ * 2 * m_.layers;
+  n_pages_ = d_.kv_pages;
+  if (n_pages_ <= 0) {
+    size_t fr = 0, tot = 0;
+    lp_check(cudaMemGetInfo(&fr, &tot), "meminfo");
+    const size_t reserve = size_t(6) << 30;
+    n_pages_ = fr > reserve ? static_cast<int64_t>((fr - reserve) / page_bytes_all) : 0;
+    n_pages_ = std::min<int64_t>(n_pages_, 1 << 20);
+  }
+  if (n_pages_ < 1) throw OutOfMemory("no HBM left for the KV pool");
+  layer_stride_ = page_elems_ * size_t(n_pages_);
+  kv_pool_ = dmalloc<bf16>(layer_stride_ * m_.layers, allocs_);
+  for (int32_t p = 0; p < n_pages_; ++p) free_pages_.insert(free_pages_.end(), p);
+  max_pages_ = static_cast<int>(std::min<int64_t>(n_pages_, 4096));
+
+  // Metadata block: device + pinned host mirror with identical layout.
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t o_sc = carve(16 * 4), o_tok = carve(size_t(t_max_) * 4), o_pos = carve(size_t(t_max_) * 4),
+               o_slot = carve(size_t(t_max_) * 4), o_qs = carve(r_max_ * 4), o_ql = carve(r_max_ * 4),
+               o_h = carve(r_max_ * 4), o_li = carve(r_max_ * 4),
+               o_pt = carve(size_t(r_max_) * max_pages_ * 4), o_w = carve(size_t(w_max_) * 8);
+  meta_bytes_ = off;
+  meta_dev_ = dmalloc<uint8_t>(meta_bytes_, allocs_);
+  lp_check(cudaMallocHost(&meta_host_, meta_bytes_), "pinned meta");
+  std::memset(meta_host_, 0, meta_bytes_);
+  auto bind = [&](void* base, Meta& m) {
+    uint8_t* b = static_cast<uint8_t*>(base);
+    m.scalars = reinterpret_cast<int*>(b + o_sc);
+    m.tokens = reinterpret_cast<int*>(b + o_tok);
+    m.positions = reinterpret_cast<int*>(b + o_pos);
+    m.slots = reinterpret_cast<int*>(b + o_slot);
+    m.q_start = reinterpret_cast<int*>(b + o_qs);
+    m.q_len = reinterpret_cast<int*>(b + o_ql);
+    m.hist = reinterpret_cast<int*>(b + o_h);
+    m.last_idx = reinterpret_cast<int*>(b + o_li);
+    m.page_table = reinterpret_cast<int*>(b + o_pt);
+    m.work = reinterpret_cast<int2*>(b + o_w);
+  };
+  bind(meta_dev_, md_);
+  bind(meta_host_, mh_);
+  lp_check(cudaMemsetAsync(meta_dev_, 0, meta_bytes_, stream_), "meta zero");
+  lp_check(cudaStreamSynchronize(stream_), "arena sync");
+}
+
+SplitPlan Instance::plan_for(int t_cap, int r_cap) const {
+  const int sms = num_sms();
+  const int h = m_.hidden, D = m_.head_dim;
+  const int qkv_out = (m_.n_q_heads + 2 * m_.n_kv_heads) * D;
+  SplitPlan p;
+  p.bn = pow2_bn(std::min(t_cap, 256));
+  const int n_tiles = (t_cap + p.bn - 1) / p.bn;
+  p.s_qkv = pick_splits(qkv_out / 128, n_tiles, h / 64, sms);
+  p.s_o = pick_splits(h / 128, n_tiles, (m_.n_q_heads * D) / 64, sms);
+  p.s_d = pick_splits(h / 128, n_tiles, m_.intermediate / 64, sms);
+  p.bn_lm = pow2_bn(std::min(std::max(r_cap, 1), 256));
+  return p;
+}
+
+const CUtensorMap& Instance::act_map(const bf16* buf, int rows, int cols, int bn) {
+  auto key = std::make_tuple(static_cast<const void*>(buf), cols, bn);
+  auto it = act_maps_.find(key);
+  if (it != act_maps_.end()) return it->second;
+  return act_maps_.emplace(key, make_tmap_bf16(buf, rows, cols, bn)).first->second;
+}
+
+void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st) {
+  const int h = m_.hidden, I = m_.intermediate, D = m_.head_dim;
+  const int nq = m_.n_q_heads, nkv = m_.n_kv_heads;
+  const int qkv_out = (nq + 2 * nkv) * D;
+  const SplitPlan p = plan_for(t_cap, r_cap);
+  const int* n_tok = md_.scalars + 0;
+  const int* n_mem = md_.scalars + 1;
+  const RowCtx rc{n_tok, t_cap, h, m_.rms_eps};
+  const int G = nq / nkv;
+  const int work_cap = std::min(w_max_, (t_cap * G + kAttnRows - 1) / kAttnRows + r_cap);
+
+  embed_rmsnorm(rc, md_.tokens, embed_, layers_[0].g_attn, x_resid_, x_norm_, st);
+  for (int l = 0; l < m_.layers; ++l) {
+    const LayerW& w = layers_[l];
+    bf16* kv_layer = kv_pool_ + layer_stride_ * l;
+    // QKV projection -> fp32 split partials.
+    GemmArgs g;
+    g.M = qkv_out; g.N = t_cap; g.K = h; g.splits = p.s_qkv; g.n_dev = n_tok;
+    g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
+    gemm_launch(w.tm_qkv, act_map(x_norm_, t_max_, h, p.bn), g, p.bn, st);
+    QkvCtx qc{n_tok, t_cap, nq, nkv, D, kPage, ws_, p.s_qkv, size_t(t_cap), w.bqkv,
+              md_.positions, md_.slots, inv_freq_, q_, kv_layer};
+    qkv_post(qc, st);
+    AttnCtx ac{md_.scalars + 2, md_.work, md_.q_start, md_.q_len, md_.hist, md_.page_table,
+               max_pages_, q_, kv_layer, attn_, nq, nkv,
+               static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)))};
+    attention_prefill(ac, D, work_cap, st);
+    // O projection + residual + RMSNorm.
+    g = GemmArgs{};
+    g.M = h; g.N = t_cap; g.K = nq * D; g.splits = p.s_o; g.n_dev = n_tok;
+    g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
+    gemm_launch(w.tm_o, act_map(attn_, t_max_, nq * D, p.bn), g, p.bn, st);
+    resid_rmsnorm(rc, ws_, p.s_o, t_cap, x_resid_, w.g_mlp, x_norm_, st);
+    // gate/up with fused SiLU*up.
+    g = GemmArgs{};
+    g.M = 2 * I; g.N = t_cap; g.K = h; g.splits = 1; g.n_dev = n_tok;
+    g.mode = kEpiSiluMul; g.out = act_; g.ldo = I;
+    gemm_launch(w.tm_gu, act_map(x_norm_, t_max_, h, p.bn), g, p.bn, st);
+    // down + residual + next RMSNorm.
+    g = GemmArgs{};
+    g.M = h; g.N = t_cap; g.K = I; g.splits = p.s_d; g.n_dev = n_tok;
+    g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
+    gemm_launch(w.tm_d, act_map(act_, t_max_, I, p.bn), g, p.bn, st);
+    const bf16* g_next = (l + 1 < m_.layers) ? layers_[l + 1].g_attn : g_final_;
+    resid_rmsnorm(rc, ws_, p.s_d, t_cap, x_resid_, g_next, x_norm_, st);
+  }
+  // Final norm already applied; LM head on the last real token per member.
+  gather_rows(n_mem, r_cap, md_.last_idx, x_norm_, x_last_, h, st);
+  GemmArgs g;
+  g.M = m_.vocab; g.N = r_cap; g.K = h; g.splits = 1; g.n_dev = n_mem;
+  g.mode = kEpiF32; g.out = logits_; g.ldo = m_.vocab;
+  gemm_launch(tm_lm_, act_map(x_last_, std::max(r_max_, 256), h, p.bn_lm), g, p.bn_lm, st);
+  argmax_rows(n_mem, r_cap, logits_, m_.vocab, next_tok_, st);
+}
+
+std::vector<int32_t> Instance::alloc_pages(int n) {
+  if (static_cast<int64_t>(free_pages_.size()) < n) {
+    throw OutOfMemory("KV page pool exhausted (" + std::to_string(free_pages_.size()) +
+                      " free, need " + std::to_string(n) + ")");
+  }
+  std::vector<int32_t> out;
+  out.reserve(n);
+  for (int i = 0; i < n; ++i) {
+    out.push_back(*free_pages_.begin());
+    free_pages_.erase(free_pages_.begin());
+  }
+  return out;
+}
+
+void Instance::ensure_capacity(Session& s, int64_t tokens) {
+  const int64_t need = (tokens + kPage - 1) / kPage;
+  if (need > max_pages_) throw ShapeMismatch("context of " + std::to_string(tokens) + " tokens exceeds page-table capacity");
+  if (need > static_cast<int64_t>(s.pages.size())) {
+    auto extra = alloc_pages(static_cast<int>(need - s.pages.size()));
+    s.pages.insert(s.pages.end(), extra.begin(), extra.end());
+  }
+}
+
+void Instance::capture_graphs(const std::vector<int64_t>& lens, const std::vector<int32_t>& depths) {
+  if (!d_.use_graphs) return;
+  lp_check(cudaSetDevice(d_.device), "set device");
+  // Warm the launch paths (function attributes, tensor-map cache) eagerly.
+  mh_.scalars[0] = mh_.scalars[1] = mh_.scalars[2] = 0;
+  lp_check(cudaMemcpyAsync(md_.scalars, mh_.scalars, 16, cudaMemcpyHostToDevice, stream_), "meta");
+  for (int64_t L : lens) {
+    for (int32_t dep : depths) {
+      const int64_t t_cap = L * dep;
+      if (t_cap > t_max_ || dep > r_max_) continue;
+      const int64_t key = graph_key(L, dep);
+      if (graphs_.count(key)) continue;
+      enqueue_forward(static_cast<int>(t_cap), dep, stream_);  // eager warm-up (no live work)
+      cudaGraph_t graph;
+      lp_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+      enqueue_forward(static_cast<int>(t_cap), dep, stream_);
+      lp_check(cudaStreamEndCapture(stream_, &graph), "end capture");
+      cudaGraphExec_t exec;
+      lp_check(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+      cudaGraphDestroy(graph);
+      graphs_[key] = exec;
+    }
+  }
+  lp_check(cudaStreamSynchronize(stream_), "capture sync");
+}
+
+void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const int32_t* tokens) {
+  lp_check(cudaSetDevice(d_.device), "set device");
+  if (n < 1) throw ShapeMismatch("empty batch");
+  if (n > r_max_) throw ShapeMismatch("batch of " + std::to_string(n) + " exceeds max_members");
+  if (shape.kind != LP_KIND_PACKED && n > shape.depth)
+    throw ShapeMismatch("member count " + std::to_string(n) + " > shape depth " + std::to_string(shape.depth));
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) {
+    if (mem[i].new_tokens < 1) throw ShapeMismatch("member with no new tokens");
+    if (shape.kind != LP_KIND_PACKED && mem[i].new_tokens > shape.l_pad)
+      throw ShapeMismatch("member length " + std::to_string(mem[i].new_tokens) + " exceeds l_pad " +
+                          std::to_string(shape.l_pad));
+    total += mem[i].new_tokens;
+  }
+  if (total > t_max_) throw ShapeMismatch("forward of " + std::to_string(total) + " tokens exceeds arena");
+
+  // Sessions / pages: positions [0, history) must be resident. Positions a
+  // member recomputes are overwritten with the same (deterministic) values.
+  for (int i = 0; i < n; ++i) {
+    Session& s = sessions_[mem[i].session_id];
+    if (s.kv_len < mem[i].history) {
+      throw std::runtime_error("session " + std::to_string(mem[i].session_id) + ": history " +
+                               std::to_string(mem[i].history) + " not resident (have " +
+                               std::to_string(s.kv_len) + ")");
+    }
+    ensure_capacity(s, mem[i].history + mem[i].new_tokens);
+  }
+
+  // Host metadata.
+  const int G = m_.n_q_heads / m_.n_kv_heads;
+  int t = 0, nw = 0;
+  for (int i = 0; i < n; ++i) {
+    const Session& s = sessions_[mem[i].session_id];
+    const int L = static_cast<int>(mem[i].new_tokens), H = static_cast<int>(mem[i].history);
+    mh_.q_start[i] = t;
+    mh_.q_len[i] = L;
+    mh_.hist[i] = H;
+    mh_.last_idx[i] = t + L - 1;
+    int* pt = mh_.page_table + size_t(i) * max_pages_;
+    for (size_t k = 0; k < s.pages.size(); ++k) pt[k] = s.pages[k];
+    for (int j = 0; j < L; ++j, ++t) {
+      const int pos = H + j;
+      mh_.tokens[t] = tokens[t];
+      mh_.positions[t] = pos;
+      mh_.slots[t] = s.pages[pos / kPage] * kPage + pos % kPage;
+    }
+    for (int r0 = 0; r0 < L * G; r0 += kAttnRows) mh_.work[nw++] = make_int2(i, r0);
+  }
+  mh_.scalars[0] = t;
+  mh_.scalars[1] = n;
+  mh_.scalars[2] = nw;
+
+  auto h2d = [&](void* dst, const void* src, size_t bytes) {
+    if (bytes) lp_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_), "meta h2d");
+  };
+  h2d(md_.scalars, mh_.scalars, 16);
+  h2d(md_.tokens, mh_.tokens, size_t(t) * 4);
+  h2d(md_.positions, mh_.positions, size_t(t) * 4);
+  h2d(md_.slots, mh_.slots, size_t(t) * 4);
+  h2d(md_.q_start, mh_.q_start, size_t(n) * 4);
+  h2d(md_.q_len, mh_.q_len, size_t(n) * 4);
+  h2d(md_.hist, mh_.hist, size_t(n) * 4);
+  h2d(md_.last_idx, mh_.last_idx, size_t(n) * 4);
+  h2d(md_.page_table, mh_.page_table, size_t(n) * max_pages_ * 4);
+  h2d(md_.work, mh_.work, size_t(nw) * 8);
+
+  lp_check(cudaEventRecord(ev_start_, stream_), "event");
+  auto it = (shape.kind == LP_KIND_GRAPH && d_.use_graphs) ? graphs_.find(graph_key(shape.l_pad, shape.depth))
+                                                           : graphs_.end();
+  if (it != graphs_.end()) {
+    lp_check(cudaGraphLaunch(it->second, stream_), "graph launch");
+  } else {
+    // Standard / packed / uncaptured: eager launch sized to the live batch.
+    const int t_cap = std::max(16, (t + 15) / 16 * 16);
+    enqueue_forward(std::min(t_cap, t_max_), n, stream_);
+  }
+  lp_check(cudaGetLastError(), "forward launch");
+  lp_check(cudaEventRecord(ev_end_, stream_), "event");
+  for (int i = 0; i < n; ++i) {
+    Session& s = sessions_[mem[i].session_id];
+    s.kv_len = std::max<int64_t>(s.kv_len, mem[i].history + mem[i].new_tokens);
+  }
+  submitted_ = true;
+  last_n_members_ = n;
+}
+
+double Instance::wait() {
+  if (!submitted_) throw std::logic_error("lp_wait without a submit");
+  lp_check(cudaEventSynchronize(ev_end_), "forward");
+  float ms = 0;
+  lp_check(cudaEventElapsedTime(&ms, ev_start_, ev_end_), "elapsed");
+  return ms;
+}
+
+void Instance::read_next_tokens(int32_t* out, int n) {
+  if (n > last_n_members_) throw ShapeMismatch("asked for more tokens than members");
+  lp_check(cudaMemcpyAsync(out, next_tok_, size_t(n) * 4, cudaMemcpyDeviceToHost, stream_), "d2h");
+  lp_check(cudaStreamSynchronize(stream_), "d2h sync");
+}
+
+void Instance::read_logits(float* out, size_t cap) {
+  const size_t need = size_t(last_n_members_) * m_.vocab;
+  if (cap < need) throw ShapeMismatch("logits buffer too small");
+  lp_check(cudaMemcpyAsync(out, logits_, need * 4, cudaMemcpyDeviceToHost, stream_), "d2h");
+  lp_check(cudaStreamSynchronize(stream_), "d2h sync");
+}
+
+void Instance::session_pages(int64_t sid, int32_t* pages, int cap, int32_t* n_pages, int64_t* kv_len) {
+  auto it = sessions_.find(sid);
+  if (it == sessions_.end()) {
+    if (n_pages) *n_pages = 0;
+    if (kv_len) *kv_len = 0;
+    return;
+  }
+  const auto& s = it->second;
+  if (n_pages) *n_pages = static_cast<int32_t>(s.pages.size());
+  if (kv_len) *kv_len = s.kv_len;
+  for (int i = 0; i < cap && i < static_cast<int>(s.pages.size()); ++i) pages[i] = s.pages[i];
+}
+
+void Instance::session_release(int64_t sid) {
+  auto it = sessions_.find(sid);
+  if (it == sessions_.end()) return;
+  for (int32_t p : it->second.pages) free_pages_.insert(p);
+  sessions_.erase(it);
+}
+
+void Instance::read_kv(int64_t sid, int layer, int64_t pos0, int64_t n, uint16_t* k, uint16_t* v) {
+  auto it = sessions_.find(sid);
+  if (it == sessions_.end()) throw ShapeMismatch("unknown session");
+  const Session& s = it->second;
+  if (layer < 0 || layer >= m_.layers || pos0 < 0 || pos0 + n > s.kv_len)
+    throw ShapeMismatch("read_kv range outside resident KV");
+  lp_check(cudaStreamSynchronize(stream_), "sync");
+  const int D = m_.head_dim, nkv = m_.n_kv_heads;
+  std::vector<uint16_t> page(page_elems_);
+  int cur = -1;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t pos = pos0 + i;
+    const int pg = s.pages[pos / kPage];
+    if (pg != cur) {
+      lp_check(cudaMemcpy(page.data(), kv_pool_ + layer_stride_ * layer + size_t(pg) * page_elems_,
+                          page_elems_ * 2, cudaMemcpyDeviceToHost), "kv d2h");
+      cur = pg;
+    }
+    const int slot = static_cast<int>(pos % kPage);
+    for (int g = 0; g < nkv; ++g) {
+      std::memcpy(k + (i * nkv + g) * D, page.data() + (size_t(0 * nkv + g) * kPage + slot) * D, D * 2);
+      std::memcpy(v + (i * nkv + g) * D, page.data() + (size_t(1 * nkv + g) * kPage + slot) * D, D * 2);
+    }
+  }
+}
+
+void Instance::migrate(Instance& src, Instance& dst, int64_t sid) {
+  auto it = src.sessions_.find(sid);
+  if (it == src.sessions_.end()) return;
+  if (std::memcmp(&src.m_, &dst.m_, sizeof(lp_model_desc)) != 0) throw ConfigError("model mismatch");
+  dst.session_release(sid);
+  Session& ss = it->second;
+  Session& ds = dst.sessions_[sid];
+  ds.pages = dst.alloc_pages(static_cast<int>(ss.pages.size()));
+  ds.kv_len = ss.kv_len;
+  lp_check(cudaStreamSynchronize(src.stream_), "src sync");
+  const size_t bytes = src.page_elems_ * 2;
+  for (int l = 0; l < src.m_.layers; ++l) {
+    for (size_t k = 0; k < ss.pages.size(); ++k) {
+      const bf16* from = src.kv_pool_ + src.layer_stride_ * l + size_t(ss.pages[k]) * src.page_elems_;
+      bf16* to = dst.kv_pool_ + dst.layer_stride_ * l + size_t(ds.pages[k]) * dst.page_elems_;
+      if (src.d_.device == dst.d_.device)
+        lp_check(cudaMemcpyAsync(to, from, bytes, cudaMemcpyDeviceToDevice, dst.stream_), "kv copy");
+      else
+        lp_check(cudaMemcpyPeerAsync(to, dst.d_.device, from, src.d_.device, bytes, dst.stream_), "kv p2p");
+    }
+  }
+  lp_check(cudaStreamSynchronize(dst.stream_), "migrate sync");
+  src.session_release(sid);
+}
+
+}  // namespace lp
+
+// ------------------------------------------------------------------ C ABI
+using lp::Instance;
+
+struct lp_instance {
+  Instance* impl;
+};
+
+extern "C" {
+
+int lp_instance_create(const lp_model_desc* model, const lp_instance_desc* desc, lp_instance** out) {
+  return lp::lp_guard([&] {
+    if (!model || !desc || !out) throw lp::ConfigError("null argument");
+    *out = nullptr;
+    auto* h = new lp_instance{nullptr};
+    try {
+      h->impl = new Instance(*model, *desc);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int lp_instance_destroy(lp_instance* inst) {
+  return lp::lp_guard([&] {
+    if (!inst) return;
+    delete inst->impl;
+    delete inst;
+  });
+}
+
+int lp_capture_graphs(lp_instance* inst, const int64_t* lengths, int32_t n_lengths, const int32_t* depths,
+                      int32_t n_depths) {
+  return lp::lp_guard([&] {
+    if (!inst) throw lp::ConfigError("null instance");
+    inst->impl->capture_graphs(std::vector<int64_t>(lengths, lengths + n_lengths),
+                               std::vector<int32_t>(depths, depths + n_depths));
+  });
+}
+
+int lp_submit(lp_instance* inst, const lp_shape* shape, const lp_member* members, int32_t n,
+              const int32_t* token_ids) {
+  return lp::lp_guard([&] {
+    if (!inst || !shape || !members || !token_ids) throw lp::ConfigError("null argument");
+    inst->impl->submit(*shape, members, n, token_ids);
+  });
+}
+
+int lp_wait(lp_instance* inst, double* service_ms) {
+  return lp::lp_guard([&] {
+    if (!inst) throw lp::ConfigError("null instance");
+    const double ms = inst->impl->wait();
+    if (service_ms) *service_ms = ms;
+  });
+}
+
+int lp_read_next_tokens(lp_instance* inst, int32_t* out, int32_t n) {
+  return lp::lp_guard([&] { inst->impl->read_next_tokens(out, n); });
+}
+
+int lp_read_logits(lp_instance* inst, float* out, size_t cap_floats) {
+  return lp::lp_guard([&] { inst->impl->read_logits(out, cap_floats); });
+}
+
+int lp_session_pages(lp_instance* inst, int64_t session_id, int32_t* pages, int32_t cap, int32_t* n_pages,
+                     int64_t* kv_len) {
+  return lp::lp_guard([&] { inst->impl->session_pages(session_id, pages, cap, n_pages, kv_len); });
+}
+
+int lp_session_release(lp_instance* inst, int64_t session_id) {
+  return lp::lp_guard([&] { inst->impl->session_release(session_id); });
+}
+
+int lp_read_kv(lp_instance* inst, int64_t session_id, int32_t layer, int64_t pos0, int64_t n, uint16_t* k_out,
+               uint16_t* v_out) {
+  return lp::lp_guard([&] { inst->impl->read_kv(session_id, layer, pos0, n, k_out, v_out); });
+}
+
+int lp_session_migrate(lp_instance* src, lp_instance* dst, int64_t session_id) {
+  return lp::lp_guard([&] { Instance::migrate(*src->impl, *dst->impl, session_id); });
+}
+
+}  // extern "C"

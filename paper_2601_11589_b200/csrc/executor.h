@@ -1,0 +1,131 @@
+// The per-GPU prefill instance behind include/laps_prefill.h.
+//
+// One Instance == one GPU == one reference `Inst` (sim.cpp:95-112). It owns:
+//   * the random-init Qwen2-style weights (bf16, generated on device from the
+//     counter-based RNG in synth.h, so the CPU oracle can regenerate them),
+//   * the paged KV pool: per layer [pages][K|V][kv_head][64 slots][head_dim]
+//     bf16, one page id spanning all layers, deterministic lowest-free-first
+//     page allocation (restated by oracle/pages.py for bit-exact page tables),
+//   * a static activation arena sized for the largest forward, shared by every
+//     captured graph,
+//   * per-(l_pad, depth) CUDA graphs (GraphGrid, scheduler.hpp:21-32) whose
+//     kernels read live token/member counts from a device metadata block, so
+//     a replay never depends on the history lengths H_i.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <set>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/laps_prefill.h"
+#include "attn.cuh"
+#include "gemm_sm100.cuh"
+#include "ops.cuh"
+
+namespace lp {
+
+struct LayerW {
+  bf16 *wqkv, *bqkv, *wo, *wgu, *wd, *g_attn, *g_mlp;
+  CUtensorMap tm_qkv, tm_o, tm_gu, tm_d;
+};
+
+struct Session {
+  std::vector<int32_t> pages;
+  int64_t kv_len = 0;
+};
+
+// Device metadata block (one allocation, regions at fixed offsets).
+struct Meta {
+  int* scalars;     // [0] n_tokens, [1] n_members, [2] n_work
+  int* tokens;      // [T]
+  int* positions;   // [T]
+  int* slots;       // [T]
+  int* q_start;     // [R]
+  int* q_len;       // [R]
+  int* hist;        // [R]
+  int* last_idx;    // [R]
+  int* page_table;  // [R, max_pages]
+  int2* work;       // [W]
+};
+
+struct SplitPlan {
+  int bn;
+  int s_qkv, s_o, s_d;
+  int bn_lm;
+};
+
+class Instance {
+ public:
+  Instance(const lp_model_desc& m, const lp_instance_desc& d);
+  ~Instance();
+
+  void capture_graphs(const std::vector<int64_t>& lens, const std::vector<int32_t>& depths);
+  void submit(const lp_shape& shape, const lp_member* members, int n, const int32_t* tokens);
+  double wait();
+  void read_next_tokens(int32_t* out, int n);
+  void read_logits(float* out, size_t cap);
+  void session_pages(int64_t sid, int32_t* pages, int cap, int32_t* n_pages, int64_t* kv_len);
+  void session_release(int64_t sid);
+  void read_kv(int64_t sid, int layer, int64_t pos0, int64_t n, uint16_t* k, uint16_t* v);
+  static void migrate(Instance& src, Instance& dst, int64_t sid);
+
+  const lp_model_desc& model() const { return m_; }
+  int device() const { return d_.device; }
+
+ private:
+  void alloc_weights();
+  void alloc_arena();
+  SplitPlan plan_for(int t_cap, int r_cap) const;
+  void enqueue_forward(int t_cap, int r_cap, cudaStream_t st);
+  const CUtensorMap& act_map(const bf16* buf, int rows, int cols, int bn);
+  std::vector<int32_t> alloc_pages(int n);
+  void ensure_capacity(Session& s, int64_t tokens);
+  int64_t graph_key(int64_t l_pad, int depth) const { return l_pad * 1024 + depth; }
+
+  lp_model_desc m_;
+  lp_instance_desc d_;
+  cudaStream_t stream_ = nullptr;
+  cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr;
+
+  // model
+  std::vector<LayerW> layers_;
+  bf16 *embed_ = nullptr, *lm_head_ = nullptr, *g_final_ = nullptr;
+  CUtensorMap tm_lm_;
+  float* inv_freq_ = nullptr;
+  std::vector<void*> allocs_;
+
+  // kv
+  bf16* kv_pool_ = nullptr;
+  size_t layer_stride_ = 0;  // elements per layer
+  size_t page_elems_ = 0;    // elements per page per layer
+  int64_t n_pages_ = 0;
+  std::set<int32_t> free_pages_;
+  std::unordered_map<int64_t, Session> sessions_;
+  int max_pages_ = 0;  // page-table row stride
+
+  // arena
+  int t_max_ = 0, r_max_ = 0, w_max_ = 0;
+  float* x_resid_ = nullptr;
+  bf16 *x_norm_ = nullptr, *q_ = nullptr, *attn_ = nullptr, *act_ = nullptr, *x_last_ = nullptr;
+  float* ws_ = nullptr;
+  size_t ws_elems_ = 0;
+  float* logits_ = nullptr;
+  int* next_tok_ = nullptr;
+  void* meta_dev_ = nullptr;
+  void* meta_host_ = nullptr;
+  size_t meta_bytes_ = 0;
+  Meta md_{}, mh_{};
+  std::map<std::tuple<const void*, int, int>, CUtensorMap> act_maps_;
+
+  // graphs
+  std::map<int64_t, cudaGraphExec_t> graphs_;
+  bool submitted_ = false;
+  int last_n_members_ = 0;
+};
+
+}  // namespace lp
