@@ -102,6 +102,8 @@ typedef struct lp_member {
 int lp_instance_create(const lp_model_desc* model, const lp_instance_desc* desc,
                        lp_instance** out);
 int lp_instance_destroy(lp_instance* inst);
+/* Model descriptor the instance was created with. */
+int lp_instance_model(lp_instance* inst, lp_model_desc* out);
 /* Capture graphs for every (length, depth) of the grid — GraphGrid,
  * scheduler.hpp:21-32. No-op when use_graphs == 0. */
 int lp_capture_graphs(lp_instance* inst, const int64_t* lengths, int32_t n_lengths,

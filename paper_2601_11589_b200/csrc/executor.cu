@@ -61,6 +61,7 @@ Instance::Instance(const lp_model_desc& m, const lp_instance_desc& d) : m_(m), d
   lp_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   lp_check(cudaEventCreate(&ev_start_), "event");
   lp_check(cudaEventCreate(&ev_end_), "event");
+  lp_check(cudaEventCreateWithFlags(&ev_h2d_, cudaEventDisableTiming), "event");
   alloc_weights();
   alloc_arena();
 }
@@ -73,6 +74,7 @@ Instance::~Instance() {
   if (meta_host_) cudaFreeHost(meta_host_);
   cudaEventDestroy(ev_start_);
   cudaEventDestroy(ev_end_);
+  cudaEventDestroy(ev_h2d_);
   cudaStreamDestroy(stream_);
 }
 
@@ -330,6 +332,9 @@ void Instance::capture_graphs(const std::vector<int64_t>& lens, const std::vecto
 
 void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const int32_t* tokens) {
   lp_check(cudaSetDevice(d_.device), "set device");
+  // The pinned staging block is reused: the previous forward's H2D copies
+  // must have drained before it is rewritten.
+  if (submitted_) lp_check(cudaEventSynchronize(ev_h2d_), "staging reuse");
   if (n < 1) throw ShapeMismatch("empty batch");
   if (n > r_max_) throw ShapeMismatch("batch of " + std::to_string(n) + " exceeds max_members");
   if (shape.kind != LP_KIND_PACKED && n > shape.depth)
@@ -394,6 +399,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   h2d(md_.page_table, mh_.page_table, size_t(n) * max_pages_ * 4);
   h2d(md_.work, mh_.work, size_t(nw) * 8);
 
+  lp_check(cudaEventRecord(ev_h2d_, stream_), "event");
   lp_check(cudaEventRecord(ev_start_, stream_), "event");
   auto it = (shape.kind == LP_KIND_GRAPH && d_.use_graphs) ? graphs_.find(graph_key(shape.l_pad, shape.depth))
                                                            : graphs_.end();
@@ -537,6 +543,13 @@ int lp_instance_destroy(lp_instance* inst) {
     if (!inst) return;
     delete inst->impl;
     delete inst;
+  });
+}
+
+int lp_instance_model(lp_instance* inst, lp_model_desc* out) {
+  return lp::lp_guard([&] {
+    if (!inst || !out) throw lp::ConfigError("null argument");
+    *out = inst->impl->model();
   });
 }
 

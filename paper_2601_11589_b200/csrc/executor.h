@@ -90,7 +90,7 @@ class Instance {
   lp_model_desc m_;
   lp_instance_desc d_;
   cudaStream_t stream_ = nullptr;
-  cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr;
+  cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr, ev_h2d_ = nullptr;
 
   // model
   std::vector<LayerW> layers_;

@@ -1,0 +1,86 @@
+"""Python mirror of the host engine's C ABI (include/laps_engine.h).
+
+`simulate(config_text, overrides, out_dir)` is the reference's
+`prefillsim simulate --config <cfg> --out <dir>` (tools/main.cpp:76-93); with
+`mode=REPLAY` / `mode=LIVE` and GPU instances, every dispatch also runs its
+real forward on B200 (see laps_engine.h for the three modes).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from pathlib import Path
+
+from . import _native as N
+from .instance import PrefillInstance
+
+COST_MODEL, REPLAY, LIVE = 0, 1, 2
+
+
+class SimStats(ctypes.Structure):
+    _fields_ = [("arrivals", ctypes.c_int64), ("completed", ctypes.c_int64), ("dispatches", ctypes.c_int64),
+                ("gpu_forwards", ctypes.c_int64), ("fill_forwards", ctypes.c_int64),
+                ("kv_migrations", ctypes.c_int64), ("real_tokens", ctypes.c_int64),
+                ("active_ms", ctypes.c_double), ("ttft_mean_ms", ctypes.c_double),
+                ("ttft_p50_ms", ctypes.c_double), ("ttft_p90_ms", ctypes.c_double),
+                ("ttft_p99_ms", ctypes.c_double), ("rps", ctypes.c_double), ("slo_violation", ctypes.c_double),
+                ("gpu_ms_total", ctypes.c_double), ("engine_wall_s", ctypes.c_double)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _declare():
+    L = N.lib()
+    if not getattr(L, "_engine_declared", False):
+        L.lp_sim_run.restype = ctypes.c_int32
+        L.lp_sim_run.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int32,
+                                 ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, ctypes.c_uint64,
+                                 ctypes.POINTER(SimStats)]
+        L.lp_sim_trace.restype = ctypes.c_int32
+        L.lp_sim_trace.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p]
+        L._engine_declared = True
+    return L
+
+
+def read_config(path: str | Path) -> str:
+    return Path(path).read_text()
+
+
+def simulate(config_text: str, overrides: str | dict = "", out_dir: str | Path = "", mode: int = COST_MODEL,
+             instances: list[PrefillInstance] | None = None, token_seed: int = 7) -> SimStats:
+    if isinstance(overrides, dict):
+        overrides = "".join(f"{k} = {v}\n" for k, v in overrides.items())
+    L = _declare()
+    insts = instances or []
+    arr = (ctypes.c_void_p * max(1, len(insts)))(*[i._h.value for i in insts])
+    st = SimStats()
+    N.check(L.lp_sim_run(config_text.encode(), overrides.encode(), str(out_dir).encode(), mode,
+                         arr if insts else None, len(insts), token_seed, ctypes.byref(st)))
+    return st
+
+
+def dump_trace(config_text: str, overrides: str | dict, path: str | Path) -> None:
+    if isinstance(overrides, dict):
+        overrides = "".join(f"{k} = {v}\n" for k, v in overrides.items())
+    N.check(_declare().lp_sim_trace(config_text.encode(), overrides.encode(), str(path).encode()))
+
+
+@dataclass
+class TraceRow:
+    id: int
+    session: int
+    turn: int
+    L: int
+    H: int
+    arrival: float
+    deadline: float | None
+
+
+def load_trace_dump(path: str | Path) -> list[TraceRow]:
+    rows = []
+    for line in Path(path).read_text().splitlines():
+        a = line.split()
+        rows.append(TraceRow(int(a[0]), int(a[1]), int(a[2]), int(a[3]), int(a[4]), float(a[5]),
+                             None if a[6] == "none" else float(a[6])))
+    return rows
