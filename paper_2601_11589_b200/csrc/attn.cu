@@ -5,6 +5,7 @@
 #include <cstdint>
 
 #include "attn.cuh"
+#include "launch.cuh"
 
 namespace lp {
 
@@ -61,8 +62,11 @@ __global__ void __launch_bounds__(128)
   uint8_t* sK = smem + kTileBytes;          // [2][64][D]
   uint8_t* sV = sK + 2 * kTileBytes;        // [2][64][D]
 
+  pdl_trigger();
   const int wi = blockIdx.x;
-  if (wi >= *c.n_work) return;
+  const bool live = wi < *c.n_work;  // written by the pre-graph H2D copy
+  pdl_wait();
+  if (!live) return;
   const int g = blockIdx.y;
   const int G = c.nq / c.nkv;
   const int2 wk = c.work[wi];
@@ -249,10 +253,10 @@ void attention_prefill(const AttnCtx& c, int head_dim, int work_cap, cudaStream_
       cudaFuncSetAttribute(attn_prefill_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       set = true;
     }
-    attn_prefill_kernel<128><<<grid, 128, smem, st>>>(c);
+    launch_k(attn_prefill_kernel<128>, grid, dim3(128), smem, st, c);
   } else {
     constexpr int smem = 5 * 64 * 64 * 2;
-    attn_prefill_kernel<64><<<grid, 128, smem, st>>>(c);
+    launch_k(attn_prefill_kernel<64>, grid, dim3(128), smem, st, c);
   }
 }
 

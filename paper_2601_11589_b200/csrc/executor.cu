@@ -142,7 +142,7 @@ void Instance::alloc_arena() {
   act_ = dmalloc<bf16>(size_t(t_max_) * I, allocs_);
   x_last_ = dmalloc<bf16>(size_t(std::max(r_max_, 256)) * h, allocs_);
   logits_ = dmalloc<float>(size_t(r_max_) * m_.vocab, allocs_);
-  next_tok_ = dmalloc<int>(r_max_, allocs_);
+  next_keys_ = dmalloc<unsigned long long>(r_max_, allocs_);
 
   // Split-K workspace: max over every capacity we may launch with.
   ws_elems_ = 0;
@@ -273,12 +273,12 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st) {
     resid_rmsnorm(rc, ws_, p.s_d, t_cap, x_resid_, g_next, x_norm_, st);
   }
   // Final norm already applied; LM head on the last real token per member.
-  gather_rows(n_mem, r_cap, md_.last_idx, x_norm_, x_last_, h, st);
+  gather_rows(n_mem, r_cap, md_.last_idx, x_norm_, x_last_, h, next_keys_, st);
   GemmArgs g;
   g.M = m_.vocab; g.N = r_cap; g.K = h; g.splits = 1; g.n_dev = n_mem;
   g.mode = kEpiF32; g.out = logits_; g.ldo = m_.vocab;
   gemm_launch(tm_lm_, act_map(x_last_, std::max(r_max_, 256), h, p.bn_lm), g, p.bn_lm, st);
-  argmax_rows(n_mem, r_cap, logits_, m_.vocab, next_tok_, st);
+  argmax_rows(n_mem, r_cap, logits_, m_.vocab, next_keys_, st);
 }
 
 std::vector<int32_t> Instance::alloc_pages(int n) {
@@ -430,8 +430,10 @@ double Instance::wait() {
 
 void Instance::read_next_tokens(int32_t* out, int n) {
   if (n > last_n_members_) throw ShapeMismatch("asked for more tokens than members");
-  lp_check(cudaMemcpyAsync(out, next_tok_, size_t(n) * 4, cudaMemcpyDeviceToHost, stream_), "d2h");
+  std::vector<unsigned long long> keys(n);
+  lp_check(cudaMemcpyAsync(keys.data(), next_keys_, size_t(n) * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
   lp_check(cudaStreamSynchronize(stream_), "d2h sync");
+  for (int i = 0; i < n; ++i) out[i] = argmax_token(keys[i]);
 }
 
 void Instance::read_logits(float* out, size_t cap) {

@@ -115,7 +115,7 @@ class Instance {
   float* ws_ = nullptr;
   size_t ws_elems_ = 0;
   float* logits_ = nullptr;
-  int* next_tok_ = nullptr;
+  unsigned long long* next_keys_ = nullptr;
   void* meta_dev_ = nullptr;
   void* meta_host_ = nullptr;
   size_t meta_bytes_ = 0;

@@ -5,6 +5,7 @@
 #include <string>
 
 #include "gemm_sm100.cuh"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace lp {
@@ -14,7 +15,8 @@ namespace {
 constexpr int kBM = 128;            // weight rows per tile (MMA M)
 constexpr int kBK = 64;             // K per stage: one 128-byte swizzle row of bf16
 constexpr int kThreads = 192;       // warp0 TMA, warp1 MMA, warps2-5 epilogue
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kSmemBudget = 196 * 1024;
+constexpr int kEpiStageBytes = 16 * 64 * 2;  // [16 tokens][64 features] bf16
 
 template <int BN>
 struct Cfg {
@@ -23,10 +25,13 @@ struct Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (kSmemBudget / kStageBytes) > 8 ? 8 : (kSmemBudget / kStageBytes);
   static constexpr int kTmemCols = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kBarBytes = 256;
+  static constexpr int kSmem = 1024 /*align*/ + kStages * kStageBytes + kBarBytes + 2 * kEpiStageBytes;
 };
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -42,10 +47,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __nv_bfloat16* epi_stage =
+      reinterpret_cast<__nv_bfloat16*>(smem + C::kStages * C::kStageBytes + C::kBarBytes);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  pdl_trigger();
 
+  // n_dev is written by the pre-graph H2D copy, never by a kernel: safe before pdl_wait.
   const int n_live = args.n_dev ? min(*args.n_dev, args.N) : args.N;
   const int m_tiles = args.M / kBM;
   const int n_tiles = (args.N + BN - 1) / BN;
@@ -89,13 +98,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_first();  // weights stream once
       const uint64_t pol_x = policy_evict_last();   // activations are re-read per m tile
-      int stage = 0;
-      uint32_t phase = 0;
+      // Weight tiles do not depend on the previous kernel: fill the pipeline
+      // with them before waiting on it (PDL), then add the activation tiles.
+      int pre = 0;
+      int pre_w = -1, pre_kb0 = 0, pre_m0 = 0, pre_n0 = 0;
       for (int w = blockIdx.x; w < units; w += gridDim.x) {
         int s, m0, n0, kb0, kb1;
         decode(w, s, m0, n0, kb0, kb1);
         if (n0 >= n_live) continue;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        pre_w = w; pre_kb0 = kb0; pre_m0 = m0; pre_n0 = n0;
+        pre = min(kb1 - kb0, C::kStages);
+        for (int i = 0; i < pre; ++i) {
+          mbar_arrive_expect_tx(&full[i], C::kStageBytes);
+          tma_load_2d(sA + i * C::kABytes, &tmA, &full[i], (kb0 + i) * kBK, m0, pol_w);
+        }
+        break;
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(sB + i * C::kBBytes, &tmB, &full[i], (pre_kb0 + i) * kBK, pre_n0, pol_x);
+      (void)pre_m0;
+      int stage = pre % C::kStages;
+      uint32_t phase = pre == C::kStages ? 1u : 0u;
+      for (int w = (pre_w >= 0 ? pre_w : units); w < units; w += gridDim.x) {
+        int s, m0, n0, kb0, kb1;
+        decode(w, s, m0, n0, kb0, kb1);
+        if (n0 >= n_live) continue;
+        for (int kb = (w == pre_w ? kb0 + pre : kb0); kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
           tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * kBK, m0, pol_w);
@@ -143,8 +172,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ----------------------------------------------------------- epilogue
     const int q = warp % 4;          // TMEM lane quarter this warp may touch
     const int row = q * 32 + lane;   // tile row == TMEM lane
+    const int et = threadIdx.x - 64; // 0..127 within the epilogue group
     int acc = 0;
     uint32_t aphase = 0;
+    int sbuf = 0;
     for (int w = blockIdx.x; w < units; w += gridDim.x) {
       int s, m0, n0, kb0, kb1;
       decode(w, s, m0, n0, kb0, kb1);
@@ -158,41 +189,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         bias = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(args.bias)[m]);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
-        if (n0 + c >= n_live) break;  // warp-uniform
+        if (n0 + c >= n_live) break;  // uniform across the epilogue group
         float v[16];
         tmem_ld16(t_addr + c, v);
         const int nbase = n0 + c;
         const int cnt = min(16, n_live - nbase);
         if (args.mode == kEpiF32Partial) {
+          // 32 lanes x consecutive m: one full 128-byte line per token.
           float* dst = args.ws + (static_cast<size_t>(s) * args.ws_stride + nbase) * args.M + m;
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             if (j < cnt) dst[static_cast<size_t>(j) * args.M] = v[j];
+        } else if (args.mode == kEpiSiluMul) {
+          // Even row = gate, odd row = up of feature m/2. Stage the 64-feature x
+          // 16-token block in smem, then write 128-byte token rows with 16-byte
+          // vector stores.
+          __nv_bfloat16* stg = epi_stage + sbuf * (16 * 64);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float u = __shfl_xor_sync(0xffffffffu, v[j], 1);
+            if ((lane & 1) == 0) {
+              // Projections are rounded to bf16 before the activation (oracle storage point).
+              const float g = __bfloat162float(__float2bfloat16_rn(v[j]));
+              const float uu = __bfloat162float(__float2bfloat16_rn(u));
+              stg[j * 64 + (row >> 1)] = __float2bfloat16_rn(silu(g) * uu);
+            }
+          }
+          epi_bar();
+          const int tj = et >> 3, seg = et & 7;
+          if (tj < cnt) {
+            const uint4 val = *reinterpret_cast<const uint4*>(stg + tj * 64 + seg * 8);
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) +
+                                 static_cast<size_t>(nbase + tj) * args.ldo + (m0 >> 1) + seg * 8;
+            *reinterpret_cast<uint4*>(dst) = val;
+          }
+          sbuf ^= 1;
         } else if (args.mode == kEpiBf16) {
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) +
                                static_cast<size_t>(nbase) * args.ldo + m;
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             if (j < cnt) dst[static_cast<size_t>(j) * args.ldo] = __float2bfloat16_rn(v[j] + bias);
-        } else if (args.mode == kEpiF32) {
+        } else {  // kEpiF32
           float* dst = reinterpret_cast<float*>(args.out) + static_cast<size_t>(nbase) * args.ldo + m;
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             if (j < cnt) dst[static_cast<size_t>(j) * args.ldo] = v[j];
-        } else {  // kEpiSiluMul: even row = gate, odd row = up of feature m/2
-          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) +
-                               static_cast<size_t>(nbase) * args.ldo + (m >> 1);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float u = __shfl_xor_sync(0xffffffffu, v[j], 1);
-            if ((lane & 1) == 0 && j < cnt) {
-              // Round the gate/up products the way the oracle does: the
-              // projections are rounded to bf16 before the activation.
-              const float g = __bfloat162float(__float2bfloat16_rn(v[j]));
-              const float uu = __bfloat162float(__float2bfloat16_rn(u));
-              dst[static_cast<size_t>(j) * args.ldo] = __float2bfloat16_rn(silu(g) * uu);
-            }
-          }
         }
       }
       tc_fence_before();
@@ -244,7 +286,7 @@ void launch_bn(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (units < grid) grid = units;
-  gemm_bf16_tn_kernel<BN><<<grid, kThreads, C::kSmem, stream>>>(tmA, tmB, a);
+  launch_k(gemm_bf16_tn_kernel<BN>, dim3(grid), dim3(kThreads), C::kSmem, stream, tmA, tmB, a);
 }
 
 }  // namespace
@@ -282,6 +324,7 @@ void gemm_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs&
     throw std::runtime_error("gemm_launch: unsupported shape M=" + std::to_string(a.M) +
                              " K=" + std::to_string(a.K) + " N=" + std::to_string(a.N));
   }
+  if (a.mode == kEpiSiluMul && (a.ldo % 8 != 0)) throw std::runtime_error("gemm_launch: SiLU ldo % 8");
   switch (bn) {
     case 16: launch_bn<16>(tmA, tmB, a, stream, max_ctas); break;
     case 32: launch_bn<32>(tmA, tmB, a, stream, max_ctas); break;

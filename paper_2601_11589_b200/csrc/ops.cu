@@ -1,5 +1,6 @@
 #include <cstdio>
 
+#include "launch.cuh"
 #include "ops.cuh"
 #include "synth.h"
 
@@ -8,6 +9,7 @@ namespace lp {
 namespace {
 
 constexpr int kRowThreads = 256;
+constexpr int kMaxVec = 8;  // float4 per thread: hidden <= 256*4*8 = 8192
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
 #pragma unroll
@@ -15,17 +17,14 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   const int w = threadIdx.x / 32, l = threadIdx.x % 32;
   if (l == 0) red[w] = v;
   __syncthreads();
-  float s = 0.f;
   if (threadIdx.x < 32) {
-    s = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+    float s = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (threadIdx.x == 0) red[32] = s;
   }
   __syncthreads();
-  const float r = red[32];
-  __syncthreads();
-  return r;
+  return red[32];
 }
 
 __global__ void init_weights_kernel(bf16* dst, size_t n, uint64_t seed, uint64_t tid, float scale,
@@ -48,14 +47,17 @@ __global__ void fill_kernel(bf16* dst, size_t n, float v) {
     dst[i] = __float2bfloat16_rn(v);
 }
 
-// One CTA per token row. h is a multiple of 4.
+// One CTA per token row.
 __global__ void __launch_bounds__(kRowThreads)
     embed_rmsnorm_kernel(RowCtx c, const int* __restrict__ tokens, const bf16* __restrict__ embed,
                          const bf16* __restrict__ gamma, float* __restrict__ x_resid,
                          bf16* __restrict__ x_norm) {
   __shared__ float red[33];
+  pdl_trigger();
   const int t = blockIdx.x;
-  if (t >= *c.n_live) return;
+  const bool live = t < *c.n_live;
+  pdl_wait();
+  if (!live) return;
   const bf16* e = embed + static_cast<size_t>(tokens[t]) * c.h;
   float* xr = x_resid + static_cast<size_t>(t) * c.h;
   float ss = 0.f;
@@ -64,125 +66,177 @@ __global__ void __launch_bounds__(kRowThreads)
     xr[i] = v;
     ss += v * v;
   }
-  const float tot = block_sum(ss, red);
-  const float inv = rsqrtf(tot / c.h + c.eps);
+  const float inv = rsqrtf(block_sum(ss, red) / c.h + c.eps);
   bf16* xn = x_norm + static_cast<size_t>(t) * c.h;
   for (int i = threadIdx.x; i < c.h; i += blockDim.x)
     xn[i] = __float2bfloat16_rn(xr[i] * inv * __bfloat162float(gamma[i]));
 }
 
+// x_resid += sum of split partials; x_norm = bf16(rmsnorm(x_resid) * gamma).
+// All of a thread's loads (residual + every split) are issued before use.
 __global__ void __launch_bounds__(kRowThreads)
     resid_rmsnorm_kernel(RowCtx c, const float* __restrict__ ws, int splits, size_t ws_stride_rows,
                          float* __restrict__ x_resid, const bf16* __restrict__ gamma,
                          bf16* __restrict__ x_norm) {
   __shared__ float red[33];
+  pdl_trigger();
   const int t = blockIdx.x;
-  if (t >= *c.n_live) return;
-  float4* xr = reinterpret_cast<float4*>(x_resid + static_cast<size_t>(t) * c.h);
+  const bool live = t < *c.n_live;
+  pdl_wait();
+  if (!live) return;
   const int h4 = c.h / 4;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < h4; i += blockDim.x) {
-    float4 v = xr[i];
-    for (int s = 0; s < splits; ++s) {
-      const float4 p = reinterpret_cast<const float4*>(
-          ws + (static_cast<size_t>(s) * ws_stride_rows + t) * c.h)[i];
-      v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
-    }
-    xr[i] = v;
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  float4* xr = reinterpret_cast<float4*>(x_resid + static_cast<size_t>(t) * c.h);
+  float4 acc[kMaxVec];
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = threadIdx.x + k * kRowThreads;
+    acc[k] = i < h4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  const float tot = block_sum(ss, red);
-  const float inv = rsqrtf(tot / c.h + c.eps);
+  for (int s = 0; s < splits; ++s) {
+    const float4* p = reinterpret_cast<const float4*>(ws + (static_cast<size_t>(s) * ws_stride_rows + t) * c.h);
+#pragma unroll
+    for (int k = 0; k < kMaxVec; ++k) {
+      const int i = threadIdx.x + k * kRowThreads;
+      if (i < h4) {
+        const float4 q = p[i];
+        acc[k].x += q.x; acc[k].y += q.y; acc[k].z += q.z; acc[k].w += q.w;
+      }
+    }
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = threadIdx.x + k * kRowThreads;
+    if (i < h4) {
+      xr[i] = acc[k];
+      ss += acc[k].x * acc[k].x + acc[k].y * acc[k].y + acc[k].z * acc[k].z + acc[k].w * acc[k].w;
+    }
+  }
+  const float inv = rsqrtf(block_sum(ss, red) / c.h + c.eps);
   __nv_bfloat162* xn = reinterpret_cast<__nv_bfloat162*>(x_norm + static_cast<size_t>(t) * c.h);
   const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(gamma);
-  for (int i = threadIdx.x; i < h4; i += blockDim.x) {
-    const float4 v = xr[i];
-    const float2 ga = __bfloat1622float2(g2[2 * i]);
-    const float2 gb = __bfloat1622float2(g2[2 * i + 1]);
-    xn[2 * i] = __floats2bfloat162_rn(v.x * inv * ga.x, v.y * inv * ga.y);
-    xn[2 * i + 1] = __floats2bfloat162_rn(v.z * inv * gb.x, v.w * inv * gb.y);
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = threadIdx.x + k * kRowThreads;
+    if (i < h4) {
+      const float2 ga = __bfloat1622float2(g2[2 * i]);
+      const float2 gb = __bfloat1622float2(g2[2 * i + 1]);
+      xn[2 * i] = __floats2bfloat162_rn(acc[k].x * inv * ga.x, acc[k].y * inv * ga.y);
+      xn[2 * i + 1] = __floats2bfloat162_rn(acc[k].z * inv * gb.x, acc[k].w * inv * gb.y);
+    }
   }
 }
 
-// One CTA per token; thread j handles rotary pair (j, j + d/2) of one head.
-__global__ void qkv_post_kernel(QkvCtx c) {
+// grid (token, pair block); one thread per rotary pair (j, j + d/2) of one head.
+constexpr int kQkvThreads = 128;
+__global__ void __launch_bounds__(kQkvThreads) qkv_post_kernel(QkvCtx c) {
+  pdl_trigger();
   const int t = blockIdx.x;
-  if (t >= *c.n_live) return;
+  const bool live = t < *c.n_live;
+  pdl_wait();
+  if (!live) return;
   const int half = c.d / 2;
-  const int qkv_out = (c.nq + 2 * c.nkv) * c.d;
-  const int pos = c.positions[t];
-  const int slot = c.slot_mapping[t];
-  const int page = slot / c.page_size, s_in = slot % c.page_size;
-  const size_t page_elems = static_cast<size_t>(2) * c.nkv * c.page_size * c.d;
-  const int n_rot_heads = c.nq + c.nkv;  // q and k heads get RoPE
   const int total = (c.nq + 2 * c.nkv) * half;
-  for (int j = threadIdx.x; j < total; j += blockDim.x) {
-    const int head = j / half, i = j % half;
-    const int c0 = head * c.d + i, c1 = c0 + half;
-    float x0 = __bfloat162float(c.bias[c0]), x1 = __bfloat162float(c.bias[c1]);
-    for (int s = 0; s < c.splits; ++s) {
+  const int j = blockIdx.y * kQkvThreads + threadIdx.x;
+  if (j >= total) return;
+  const int qkv_out = (c.nq + 2 * c.nkv) * c.d;
+  const int head = j / half, i = j % half;
+  const int c0 = head * c.d + i, c1 = c0 + half;
+  float x0 = __bfloat162float(c.bias[c0]), x1 = __bfloat162float(c.bias[c1]);
+  float p0[8], p1[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    if (s < c.splits) {
       const float* row = c.ws + (static_cast<size_t>(s) * c.ws_stride_rows + t) * qkv_out;
-      x0 += row[c0];
-      x1 += row[c1];
+      p0[s] = row[c0];
+      p1[s] = row[c1];
     }
-    if (head < n_rot_heads) {
-      float sn, cs;
-      sincosf(static_cast<float>(pos) * c.inv_freq[i], &sn, &cs);
-      const float r0 = x0 * cs - x1 * sn;
-      const float r1 = x1 * cs + x0 * sn;
-      x0 = r0;
-      x1 = r1;
+  }
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    if (s < c.splits) {
+      x0 += p0[s];
+      x1 += p1[s];
     }
-    const bf16 b0 = __float2bfloat16_rn(x0), b1 = __float2bfloat16_rn(x1);
-    if (head < c.nq) {
-      bf16* q = c.q_out + static_cast<size_t>(t) * c.nq * c.d + head * c.d;
-      q[i] = b0;
-      q[i + half] = b1;
-    } else {
-      const bool is_v = head >= c.nq + c.nkv;
-      const int g = is_v ? head - c.nq - c.nkv : head - c.nq;
-      bf16* dst = c.kv_layer + page * page_elems +
-                  ((static_cast<size_t>(is_v ? 1 : 0) * c.nkv + g) * c.page_size + s_in) * c.d;
-      dst[i] = b0;
-      dst[i + half] = b1;
-    }
+  }
+  if (head < c.nq + c.nkv) {  // RoPE on q and k heads (rotate-half pairing)
+    float sn, cs;
+    sincosf(static_cast<float>(c.positions[t]) * c.inv_freq[i], &sn, &cs);
+    const float r0 = x0 * cs - x1 * sn;
+    const float r1 = x1 * cs + x0 * sn;
+    x0 = r0;
+    x1 = r1;
+  }
+  const bf16 b0 = __float2bfloat16_rn(x0), b1 = __float2bfloat16_rn(x1);
+  if (head < c.nq) {
+    bf16* q = c.q_out + static_cast<size_t>(t) * c.nq * c.d + head * c.d;
+    q[i] = b0;
+    q[i + half] = b1;
+  } else {
+    const int slot = c.slot_mapping[t];
+    const int page = slot / c.page_size, s_in = slot % c.page_size;
+    const size_t page_elems = static_cast<size_t>(2) * c.nkv * c.page_size * c.d;
+    const bool is_v = head >= c.nq + c.nkv;
+    const int g = is_v ? head - c.nq - c.nkv : head - c.nq;
+    bf16* dst = c.kv_layer + page * page_elems +
+                ((static_cast<size_t>(is_v ? 1 : 0) * c.nkv + g) * c.page_size + s_in) * c.d;
+    dst[i] = b0;
+    dst[i + half] = b1;
   }
 }
 
-__global__ void gather_rows_kernel(const int* n_rows, const int* idx, const bf16* src, bf16* dst,
-                                   int h) {
+// Copies the last-token rows for the LM head and resets the argmax keys.
+__global__ void gather_rows_kernel(const int* n_rows, const int* idx, const bf16* src, bf16* dst, int h,
+                                   unsigned long long* keys) {
+  pdl_trigger();
   const int r = blockIdx.x;
-  if (r >= *n_rows) return;
+  const bool live = r < *n_rows;
+  pdl_wait();
+  if (!live) return;
+  if (threadIdx.x == 0) keys[r] = 0ull;
   const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<size_t>(idx[r]) * h);
   uint4* d = reinterpret_cast<uint4*>(dst + static_cast<size_t>(r) * h);
   for (int i = threadIdx.x; i < h / 8; i += blockDim.x) d[i] = s[i];
 }
 
-__global__ void argmax_kernel(const int* n_rows, const float* logits, int vocab, int* out) {
+// Order-preserving key: larger value wins, ties -> lower index.
+__device__ __forceinline__ unsigned long long argmax_key(float v, int j) {
+  uint32_t u = __float_as_uint(v);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return (static_cast<unsigned long long>(u) << 32) | static_cast<uint32_t>(0x7fffffff - j);
+}
+
+constexpr int kArgmaxChunks = 32;
+__global__ void __launch_bounds__(256)
+    argmax_kernel(const int* n_rows, const float* logits, int vocab, unsigned long long* keys) {
+  pdl_trigger();
   const int r = blockIdx.x;
-  if (r >= *n_rows) return;
+  const bool live = r < *n_rows;
+  pdl_wait();
+  if (!live) return;
   const float* row = logits + static_cast<size_t>(r) * vocab;
-  float best = -INFINITY;
-  int bi = 0x7fffffff;
-  for (int j = threadIdx.x; j < vocab; j += blockDim.x) {
-    const float v = row[j];
-    if (v > best || (v == best && j < bi)) { best = v; bi = j; }
+  const int per = ((vocab + kArgmaxChunks - 1) / kArgmaxChunks + 3) & ~3;
+  const int b = blockIdx.y * per, e = min(vocab, b + per);
+  unsigned long long best = 0;
+  for (int j = b + 4 * threadIdx.x; j < e; j += 4 * blockDim.x) {
+    if (j + 3 < e) {
+      const float4 v = *reinterpret_cast<const float4*>(row + j);
+      best = max(best, argmax_key(v.x, j));
+      best = max(best, argmax_key(v.y, j + 1));
+      best = max(best, argmax_key(v.z, j + 2));
+      best = max(best, argmax_key(v.w, j + 3));
+    } else {
+      for (int k = j; k < e; ++k) best = max(best, argmax_key(row[k], k));
+    }
   }
-  __shared__ float sv[32];
-  __shared__ int si[32];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-  }
-  const int w = threadIdx.x / 32;
-  if (threadIdx.x % 32 == 0) { sv[w] = best; si[w] = bi; }
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  __shared__ unsigned long long sm[8];
+  if (threadIdx.x % 32 == 0) sm[threadIdx.x / 32] = best;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int k = 1; k < blockDim.x / 32; ++k)
-      if (sv[k] > best || (sv[k] == best && si[k] < bi)) { best = sv[k]; bi = si[k]; }
-    out[r] = bi;
+    for (int k = 1; k < blockDim.x / 32; ++k) best = max(best, sm[k]);
+    atomicMax(keys + r, best);
   }
 }
 
@@ -199,27 +253,30 @@ void fill_bf16(bf16* dst, size_t n, float v, cudaStream_t st) {
 
 void embed_rmsnorm(const RowCtx& c, const int* tokens, const bf16* embed, const bf16* gamma,
                    float* x_resid, bf16* x_norm, cudaStream_t st) {
-  embed_rmsnorm_kernel<<<c.t_cap, kRowThreads, 0, st>>>(c, tokens, embed, gamma, x_resid, x_norm);
+  launch_k(embed_rmsnorm_kernel, dim3(c.t_cap), dim3(kRowThreads), 0, st, c, tokens, embed, gamma,
+           x_resid, x_norm);
 }
 
 void resid_rmsnorm(const RowCtx& c, const float* ws, int splits, size_t ws_stride_rows,
                    float* x_resid, const bf16* gamma, bf16* x_norm, cudaStream_t st) {
-  resid_rmsnorm_kernel<<<c.t_cap, kRowThreads, 0, st>>>(c, ws, splits, ws_stride_rows, x_resid,
-                                                        gamma, x_norm);
+  launch_k(resid_rmsnorm_kernel, dim3(c.t_cap), dim3(kRowThreads), 0, st, c, ws, splits, ws_stride_rows,
+           x_resid, gamma, x_norm);
 }
 
 void qkv_post(const QkvCtx& c, cudaStream_t st) {
-  qkv_post_kernel<<<c.t_cap, 256, 0, st>>>(c);
+  const int pairs = (c.nq + 2 * c.nkv) * (c.d / 2);
+  launch_k(qkv_post_kernel, dim3(c.t_cap, (pairs + kQkvThreads - 1) / kQkvThreads), dim3(kQkvThreads), 0,
+           st, c);
 }
 
 void gather_rows(const int* n_rows, int r_cap, const int* idx, const bf16* src, bf16* dst, int h,
-                 cudaStream_t st) {
-  gather_rows_kernel<<<r_cap, 128, 0, st>>>(n_rows, idx, src, dst, h);
+                 unsigned long long* argmax_keys, cudaStream_t st) {
+  launch_k(gather_rows_kernel, dim3(r_cap), dim3(128), 0, st, n_rows, idx, src, dst, h, argmax_keys);
 }
 
-void argmax_rows(const int* n_rows, int r_cap, const float* logits, int vocab, int* out,
+void argmax_rows(const int* n_rows, int r_cap, const float* logits, int vocab, unsigned long long* keys,
                  cudaStream_t st) {
-  argmax_kernel<<<r_cap, 1024, 0, st>>>(n_rows, logits, vocab, out);
+  launch_k(argmax_kernel, dim3(r_cap, kArgmaxChunks), dim3(256), 0, st, n_rows, logits, vocab, keys);
 }
 
 }  // namespace lp

@@ -52,11 +52,15 @@ struct QkvCtx {
 // reduce splits + bias; RoPE(q, k); q -> q_out; k, v -> paged cache
 void qkv_post(const QkvCtx& c, cudaStream_t st);
 
-// x_last[r] = x_norm[last_idx[r]]
+// x_last[r] = x_norm[last_idx[r]]; also zeroes argmax_keys[r].
 void gather_rows(const int* n_rows, int r_cap, const int* idx, const bf16* src, bf16* dst, int h,
+                 unsigned long long* argmax_keys, cudaStream_t st);
+// keys[r] = max over j of an order-preserving (logit, -j) key: the greedy
+// first token is 0x7fffffff - (key & 0xffffffff) (lowest index on ties).
+void argmax_rows(const int* n_rows, int r_cap, const float* logits, int vocab, unsigned long long* keys,
                  cudaStream_t st);
-// out[r] = argmax_j logits[r, j] (lowest index on ties)
-void argmax_rows(const int* n_rows, int r_cap, const float* logits, int vocab, int* out,
-                 cudaStream_t st);
+inline int32_t argmax_token(unsigned long long key) {
+  return static_cast<int32_t>(0x7fffffffu - static_cast<uint32_t>(key & 0xffffffffull));
+}
 
 }  // namespace lp

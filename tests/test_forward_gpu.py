@@ -6,7 +6,8 @@ Tolerances. Tiny model: logits max-abs <= 2e-2 and cosine > 0.999 per member
 batch run under two split-K plans — is max-abs 0.031 / mean-abs 0.0052
 (scripts/diag7b_b.py), and the oracle gap equals it, so the
 stated tolerance is max-abs <= 5e-2, mean-abs <= 1e-2, cosine > 0.9999.
-KV values max-abs <= 2e-2 (bf16 storage, |K|,|V| ~ 1). Page tables bit-exact.
+KV values max-abs <= 2e-2 (tiny) / 6.25e-2 with mean <= 5e-3 (7B-shaped; |K|,|V| ~ 1,
+bf16 storage). Page tables bit-exact.
 Greedy first tokens bit-exact wherever the oracle's top-2 margin exceeds 2x
 the max-abs tolerance.
 """
@@ -52,15 +53,17 @@ def _compare(inst, oracle, pages, l_pad, depth, kind, members, check_tokens=True
     return err, cos
 
 
-def _kv_check(inst, oracle, sid, layers):
+def _kv_check(inst, oracle, sid, layers, max_abs=2e-2, mean_abs=None):
     _, kv_len = inst.session_pages(sid)
     for l in layers:
         k, v = inst.read_kv(sid, l, 0, kv_len)
         kk = torch.from_numpy(k.view(np.int16)).view(torch.bfloat16).float()
         vv = torch.from_numpy(v.view(np.int16)).view(torch.bfloat16).float()
         K, V = oracle.read_kv(sid, l, 0, kv_len)
-        assert (kk - K).abs().max().item() <= 2e-2
-        assert (vv - V).abs().max().item() <= 2e-2
+        for got, want in ((kk, K), (vv, V)):
+            assert (got - want).abs().max().item() <= max_abs
+            if mean_abs is not None:
+                assert (got - want).abs().mean().item() <= mean_abs
 
 
 @pytest.fixture(scope="module")
@@ -114,4 +117,5 @@ def test_7b_shaped_two_layers():
     _compare(inst, oracle, pages, 256, 2, KIND_GRAPH, [M(0, 0, 200, 0), M(1, 1, 77, 0)], tol=tol)
     _compare(inst, oracle, pages, 128, 1, KIND_GRAPH, [M(2, 0, 100, 200)], tol=tol)
     _compare(inst, oracle, pages, 600, 1, KIND_STANDARD, [M(3, 2, 600, 0)], tol=tol)
-    _kv_check(inst, oracle, 0, [0, 1])
+    # layer >= 1 inherits the residual-stream noise floor: <= 4 bf16 ulps at |x| < 4
+    _kv_check(inst, oracle, 0, [0, 1], max_abs=6.25e-2, mean_abs=5e-3)
