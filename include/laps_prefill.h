@@ -125,6 +125,14 @@ int lp_read_next_tokens(lp_instance* inst, int32_t* out, int32_t n);
 /* fp32 logits [n, vocab] of the last submit (debug/parity; large). */
 int lp_read_logits(lp_instance* inst, float* out, size_t cap_floats);
 
+/* Host->device bytes copied by the last lp_submit (token ids + metadata)
+ * and device->host bytes of the last lp_read_next_tokens. */
+int lp_last_io(lp_instance* inst, int64_t* h2d_bytes, int64_t* d2h_bytes);
+/* Device-side timing on the instance stream (CUDA events): record `slot`
+ * (0..7); elapsed ms between two recorded slots (blocks on slot_b). */
+int lp_timer_record(lp_instance* inst, int32_t slot);
+int lp_timer_elapsed(lp_instance* inst, int32_t slot_a, int32_t slot_b, double* ms);
+
 /* ---- paged KV cache ---- */
 /* Page table of a session: up to `cap` page ids; *kv_len = resident tokens. */
 int lp_session_pages(lp_instance* inst, int64_t session_id, int32_t* pages, int32_t cap,

@@ -75,7 +75,9 @@ PUBLIC_SYMBOLS = [
     "lp_instance_create", "lp_instance_destroy", "lp_capture_graphs", "lp_submit", "lp_wait",
     "lp_read_next_tokens", "lp_read_logits", "lp_session_pages", "lp_session_release",
     "lp_read_kv", "lp_session_migrate", "lp_synth_token", "lp_last_error", "lp_version",
+    "lp_instance_model", "lp_timer_record", "lp_timer_elapsed", "lp_last_io",
 ]
+ENGINE_SYMBOLS = ["lp_sim_run", "lp_sim_trace"]  # include/laps_engine.h
 
 
 def _declare(L: ctypes.CDLL) -> None:
@@ -102,5 +104,10 @@ def _declare(L: ctypes.CDLL) -> None:
     sig("lp_session_release", c_i32, vp, c_i64)
     sig("lp_read_kv", c_i32, vp, c_i64, c_i32, c_i64, c_i64, vp, vp)
     sig("lp_session_migrate", c_i32, vp, vp, c_i64)
+    sig("lp_instance_model", c_i32, vp, ctypes.POINTER(ModelDesc))
+    sig("lp_timer_record", c_i32, vp, c_i32)
+    sig("lp_last_io", c_i32, vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64))
+    sig("lp_timer_elapsed", c_i32, vp, c_i32, c_i32, ctypes.POINTER(c_f64))
+    sig("lpk_time_gemm", c_i32, vp, c_i32, c_i32, c_i32, c_i32, c_i32, ctypes.POINTER(c_f64))
     # kernel-level test hooks (include/laps_prefill_testing.h)
-    sig("lpk_gemm", c_i32, vp, vp, vp, vp, vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, vp, vp)
+    sig("lpk_gemm", c_i32, vp, vp, vp, vp, vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, vp, vp, c_i32)

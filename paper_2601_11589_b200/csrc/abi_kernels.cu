@@ -13,10 +13,10 @@ using namespace lp;
 extern "C" {
 
 int lpk_gemm(const void* W, const void* X, void* out, float* ws, const void* bias, int M, int N,
-             int K, int splits, int mode, int bn, int ldo, const int* n_dev, void* stream) {
+             int K, int splits, int mode, int bn, int ldo, const int* n_dev, void* stream, int pair) {
   return lp_guard([&] {
     const CUtensorMap ta = make_tmap_bf16(W, M, K, 128);
-    const CUtensorMap tb = make_tmap_bf16(X, N, K, bn);
+    const CUtensorMap tb = make_tmap_bf16(X, N, K, gemm_b_box_rows(bn, pair));
     GemmArgs a;
     a.M = M;
     a.N = N;
@@ -29,7 +29,7 @@ int lpk_gemm(const void* W, const void* X, void* out, float* ws, const void* bia
     a.bias = bias;
     a.ws = ws;
     a.ws_stride = N;
-    gemm_launch(ta, tb, a, bn, static_cast<cudaStream_t>(stream));
+    gemm_launch(ta, tb, a, bn, static_cast<cudaStream_t>(stream), 0, pair);
     lp_check(cudaGetLastError(), "gemm launch");
   });
 }

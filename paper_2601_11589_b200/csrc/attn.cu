@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(128)
   const int L = c.q_len[r], H = c.hist[r], qs = c.q_start[r];
   const int rows_total = L * G;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-  const int* pages = c.page_table + static_cast<size_t>(r) * c.max_pages;
+  const int* pages = c.page_list + c.page_off[r];
   const size_t page_elems = static_cast<size_t>(2) * c.nkv * kAttnPage * D;
   const size_t ld_q = static_cast<size_t>(c.nq) * D;
 

@@ -25,8 +25,8 @@ struct AttnCtx {
   const int* q_start;     // [R]: packed index of member's first new token
   const int* q_len;       // [R]: L_r
   const int* hist;        // [R]: H_r
-  const int* page_table;  // [R, max_pages]
-  int max_pages;
+  const int* page_list;   // flattened page ids of every member
+  const int* page_off;    // [R]: member r's pages start at page_list[page_off[r]]
   const __nv_bfloat16* q;        // [T, nq*d]
   const __nv_bfloat16* kv_layer; // this layer's paged cache
   __nv_bfloat16* out;            // [T, nq*d]

@@ -37,12 +37,20 @@ int pow2_bn(int t) {
   return b;
 }
 
-int pick_splits(int m_tiles, int n_tiles, int num_kb, int sms) {
-  const int units = m_tiles * n_tiles;
-  if (units >= sms) return 1;
-  int s = sms / units;
-  s = std::min(s, std::max(1, num_kb / 4));
-  return std::max(1, std::min(s, 8));
+// bn: smallest power-of-two tile >= tokens (<= 256). CTA pairs
+// (cta_group::2) once the token tile is >= 128 wide: the activation tile is
+// then re-read per 256 weight rows instead of per 128. Split-K only when the
+// (m, n) tiles cannot occupy every SM (pair) and only for fp32-partial outputs.
+GemmPlan plan_gemm(int M, int K, int t_cap, bool allow_split, int sms) {
+  GemmPlan p;
+  p.bn = pow2_bn(std::min(t_cap, 256));
+  p.pair = (p.bn >= 128 && M % 256 == 0) ? 2 : 1;
+  const int workers = sms / p.pair;
+  const int units = (M / (128 * p.pair)) * ((t_cap + p.bn - 1) / p.bn);
+  if (allow_split && units < workers) {
+    p.splits = std::max(1, std::min({workers / units, std::max(1, (K / 64) / 4), 8}));
+  }
+  return p;
 }
 
 }  // namespace
@@ -75,6 +83,8 @@ Instance::~Instance() {
   cudaEventDestroy(ev_start_);
   cudaEventDestroy(ev_end_);
   cudaEventDestroy(ev_h2d_);
+  for (cudaEvent_t e : timers_)
+    if (e) cudaEventDestroy(e);
   cudaStreamDestroy(stream_);
 }
 
@@ -148,8 +158,8 @@ void Instance::alloc_arena() {
   ws_elems_ = 0;
   for (int t = 16; t <= t_max_; t += 16) {
     const SplitPlan p = plan_for(t, 1);
-    const size_t mx = std::max<size_t>({size_t(p.s_qkv) * qkv_out, size_t(p.s_o) * h,
-                                        size_t(p.s_d) * h});
+    const size_t mx = std::max<size_t>({size_t(p.qkv.splits) * qkv_out, size_t(p.o.splits) * h,
+                                        size_t(p.d.splits) * h});
     ws_elems_ = std::max(ws_elems_, mx * size_t(t));
   }
   ws_ = dmalloc<float>(ws_elems_, allocs_);
@@ -180,7 +190,7 @@ void Instance::alloc_arena() {
   };
   const size_t o_sc = carve(16 * 4), o_tok = carve(size_t(t_max_) * 4), o_pos = carve(size_t(t_max_) * 4),
                o_slot = carve(size_t(t_max_) * 4), o_qs = carve(r_max_ * 4), o_ql = carve(r_max_ * 4),
-               o_h = carve(r_max_ * 4), o_li = carve(r_max_ * 4),
+               o_h = carve(r_max_ * 4), o_li = carve(r_max_ * 4), o_po = carve(r_max_ * 4),
                o_pt = carve(size_t(r_max_) * max_pages_ * 4), o_w = carve(size_t(w_max_) * 8);
   meta_bytes_ = off;
   meta_dev_ = dmalloc<uint8_t>(meta_bytes_, allocs_);
@@ -197,6 +207,7 @@ void Instance::alloc_arena() {
     m.hist = reinterpret_cast<int*>(b + o_h);
     m.last_idx = reinterpret_cast<int*>(b + o_li);
     m.page_table = reinterpret_cast<int*>(b + o_pt);
+    m.page_off = reinterpret_cast<int*>(b + o_po);
     m.work = reinterpret_cast<int2*>(b + o_w);
   };
   bind(meta_dev_, md_);
@@ -210,20 +221,25 @@ SplitPlan Instance::plan_for(int t_cap, int r_cap) const {
   const int h = m_.hidden, D = m_.head_dim;
   const int qkv_out = (m_.n_q_heads + 2 * m_.n_kv_heads) * D;
   SplitPlan p;
-  p.bn = pow2_bn(std::min(t_cap, 256));
-  const int n_tiles = (t_cap + p.bn - 1) / p.bn;
-  p.s_qkv = pick_splits(qkv_out / 128, n_tiles, h / 64, sms);
-  p.s_o = pick_splits(h / 128, n_tiles, (m_.n_q_heads * D) / 64, sms);
-  p.s_d = pick_splits(h / 128, n_tiles, m_.intermediate / 64, sms);
-  p.bn_lm = pow2_bn(std::min(std::max(r_cap, 1), 256));
+  p.qkv = plan_gemm(qkv_out, h, t_cap, true, sms);
+  p.o = plan_gemm(h, m_.n_q_heads * D, t_cap, true, sms);
+  p.gu = plan_gemm(2 * m_.intermediate, h, t_cap, false, sms);
+  p.d = plan_gemm(h, m_.intermediate, t_cap, true, sms);
+  p.lm = plan_gemm(m_.vocab, h, std::max(r_cap, 1), false, sms);
   return p;
 }
 
-const CUtensorMap& Instance::act_map(const bf16* buf, int rows, int cols, int bn) {
-  auto key = std::make_tuple(static_cast<const void*>(buf), cols, bn);
+const CUtensorMap& Instance::act_map(const bf16* buf, int rows, int cols, int box_rows) {
+  auto key = std::make_tuple(static_cast<const void*>(buf), cols, box_rows);
   auto it = act_maps_.find(key);
   if (it != act_maps_.end()) return it->second;
-  return act_maps_.emplace(key, make_tmap_bf16(buf, rows, cols, bn)).first->second;
+  return act_maps_.emplace(key, make_tmap_bf16(buf, rows, cols, box_rows)).first->second;
+}
+
+void Instance::gemm(const CUtensorMap& tm_w, const GemmPlan& p, GemmArgs g, const bf16* x, int x_rows,
+                    cudaStream_t st) {
+  g.splits = p.splits;
+  gemm_launch(tm_w, act_map(x, x_rows, g.K, gemm_b_box_rows(p.bn, p.pair)), g, p.bn, st, 0, p.pair);
 }
 
 void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st) {
@@ -243,41 +259,41 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st) {
     bf16* kv_layer = kv_pool_ + layer_stride_ * l;
     // QKV projection -> fp32 split partials.
     GemmArgs g;
-    g.M = qkv_out; g.N = t_cap; g.K = h; g.splits = p.s_qkv; g.n_dev = n_tok;
+    g.M = qkv_out; g.N = t_cap; g.K = h; g.n_dev = n_tok;
     g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
-    gemm_launch(w.tm_qkv, act_map(x_norm_, t_max_, h, p.bn), g, p.bn, st);
-    QkvCtx qc{n_tok, t_cap, nq, nkv, D, kPage, ws_, p.s_qkv, size_t(t_cap), w.bqkv,
+    gemm(w.tm_qkv, p.qkv, g, x_norm_, t_max_, st);
+    QkvCtx qc{n_tok, t_cap, nq, nkv, D, kPage, ws_, p.qkv.splits, size_t(t_cap), w.bqkv,
               md_.positions, md_.slots, inv_freq_, q_, kv_layer};
     qkv_post(qc, st);
     AttnCtx ac{md_.scalars + 2, md_.work, md_.q_start, md_.q_len, md_.hist, md_.page_table,
-               max_pages_, q_, kv_layer, attn_, nq, nkv,
+               md_.page_off, q_, kv_layer, attn_, nq, nkv,
                static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)))};
     attention_prefill(ac, D, work_cap, st);
     // O projection + residual + RMSNorm.
     g = GemmArgs{};
-    g.M = h; g.N = t_cap; g.K = nq * D; g.splits = p.s_o; g.n_dev = n_tok;
+    g.M = h; g.N = t_cap; g.K = nq * D; g.n_dev = n_tok;
     g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
-    gemm_launch(w.tm_o, act_map(attn_, t_max_, nq * D, p.bn), g, p.bn, st);
-    resid_rmsnorm(rc, ws_, p.s_o, t_cap, x_resid_, w.g_mlp, x_norm_, st);
+    gemm(w.tm_o, p.o, g, attn_, t_max_, st);
+    resid_rmsnorm(rc, ws_, p.o.splits, t_cap, x_resid_, w.g_mlp, x_norm_, st);
     // gate/up with fused SiLU*up.
     g = GemmArgs{};
-    g.M = 2 * I; g.N = t_cap; g.K = h; g.splits = 1; g.n_dev = n_tok;
+    g.M = 2 * I; g.N = t_cap; g.K = h; g.n_dev = n_tok;
     g.mode = kEpiSiluMul; g.out = act_; g.ldo = I;
-    gemm_launch(w.tm_gu, act_map(x_norm_, t_max_, h, p.bn), g, p.bn, st);
+    gemm(w.tm_gu, p.gu, g, x_norm_, t_max_, st);
     // down + residual + next RMSNorm.
     g = GemmArgs{};
-    g.M = h; g.N = t_cap; g.K = I; g.splits = p.s_d; g.n_dev = n_tok;
+    g.M = h; g.N = t_cap; g.K = I; g.n_dev = n_tok;
     g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
-    gemm_launch(w.tm_d, act_map(act_, t_max_, I, p.bn), g, p.bn, st);
+    gemm(w.tm_d, p.d, g, act_, t_max_, st);
     const bf16* g_next = (l + 1 < m_.layers) ? layers_[l + 1].g_attn : g_final_;
-    resid_rmsnorm(rc, ws_, p.s_d, t_cap, x_resid_, g_next, x_norm_, st);
+    resid_rmsnorm(rc, ws_, p.d.splits, t_cap, x_resid_, g_next, x_norm_, st);
   }
   // Final norm already applied; LM head on the last real token per member.
   gather_rows(n_mem, r_cap, md_.last_idx, x_norm_, x_last_, h, next_keys_, st);
   GemmArgs g;
-  g.M = m_.vocab; g.N = r_cap; g.K = h; g.splits = 1; g.n_dev = n_mem;
+  g.M = m_.vocab; g.N = r_cap; g.K = h; g.n_dev = n_mem;
   g.mode = kEpiF32; g.out = logits_; g.ldo = m_.vocab;
-  gemm_launch(tm_lm_, act_map(x_last_, std::max(r_max_, 256), h, p.bn_lm), g, p.bn_lm, st);
+  gemm(tm_lm_, p.lm, g, x_last_, std::max(r_max_, 256), st);
   argmax_rows(n_mem, r_cap, logits_, m_.vocab, next_keys_, st);
 }
 
@@ -363,7 +379,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
 
   // Host metadata.
   const int G = m_.n_q_heads / m_.n_kv_heads;
-  int t = 0, nw = 0;
+  int t = 0, nw = 0, np = 0;
   for (int i = 0; i < n; ++i) {
     const Session& s = sessions_[mem[i].session_id];
     const int L = static_cast<int>(mem[i].new_tokens), H = static_cast<int>(mem[i].history);
@@ -371,8 +387,10 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
     mh_.q_len[i] = L;
     mh_.hist[i] = H;
     mh_.last_idx[i] = t + L - 1;
-    int* pt = mh_.page_table + size_t(i) * max_pages_;
-    for (size_t k = 0; k < s.pages.size(); ++k) pt[k] = s.pages[k];
+    // Ragged page list: only the pages covering [0, H + L) are shipped.
+    mh_.page_off[i] = np;
+    const int used = (H + L + kPage - 1) / kPage;
+    for (int k = 0; k < used; ++k) mh_.page_table[np++] = s.pages[k];
     for (int j = 0; j < L; ++j, ++t) {
       const int pos = H + j;
       mh_.tokens[t] = tokens[t];
@@ -385,8 +403,10 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   mh_.scalars[1] = n;
   mh_.scalars[2] = nw;
 
+  last_h2d_bytes_ = 0;
   auto h2d = [&](void* dst, const void* src, size_t bytes) {
     if (bytes) lp_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_), "meta h2d");
+    last_h2d_bytes_ += bytes;
   };
   h2d(md_.scalars, mh_.scalars, 16);
   h2d(md_.tokens, mh_.tokens, size_t(t) * 4);
@@ -396,7 +416,8 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   h2d(md_.q_len, mh_.q_len, size_t(n) * 4);
   h2d(md_.hist, mh_.hist, size_t(n) * 4);
   h2d(md_.last_idx, mh_.last_idx, size_t(n) * 4);
-  h2d(md_.page_table, mh_.page_table, size_t(n) * max_pages_ * 4);
+  h2d(md_.page_off, mh_.page_off, size_t(n) * 4);
+  h2d(md_.page_table, mh_.page_table, size_t(np) * 4);
   h2d(md_.work, mh_.work, size_t(nw) * 8);
 
   lp_check(cudaEventRecord(ev_h2d_, stream_), "event");
@@ -420,6 +441,60 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   last_n_members_ = n;
 }
 
+void Instance::timer_record(int slot) {
+  if (slot < 0 || slot >= kTimerSlots) throw ShapeMismatch("timer slot out of range");
+  if (!timers_[slot]) lp_check(cudaEventCreate(&timers_[slot]), "timer event");
+  lp_check(cudaEventRecord(timers_[slot], stream_), "timer record");
+}
+
+double Instance::timer_elapsed(int a, int b) {
+  if (a < 0 || b < 0 || a >= kTimerSlots || b >= kTimerSlots || !timers_[a] || !timers_[b])
+    throw ShapeMismatch("timer slot not recorded");
+  lp_check(cudaEventSynchronize(timers_[b]), "timer sync");
+  float ms = 0;
+  lp_check(cudaEventElapsedTime(&ms, timers_[a], timers_[b]), "timer elapsed");
+  return ms;
+}
+
+double Instance::time_gemm(int layer, int which, int t_cap, int n_live, int iters) {
+  if (layer < 0 || layer >= m_.layers || t_cap < 1 || t_cap > t_max_ || n_live > t_cap || iters < 1)
+    throw ShapeMismatch("time_gemm: bad arguments");
+  lp_check(cudaSetDevice(d_.device), "set device");
+  const int h = m_.hidden, I = m_.intermediate, D = m_.head_dim;
+  const int qkv_out = (m_.n_q_heads + 2 * m_.n_kv_heads) * D;
+  const SplitPlan sp = plan_for(t_cap, std::min(t_cap, r_max_));
+  const LayerW& w = layers_[layer];
+  if (submitted_) lp_check(cudaEventSynchronize(ev_h2d_), "staging reuse");
+  mh_.scalars[0] = n_live;
+  mh_.scalars[1] = std::min(n_live, r_max_);
+  lp_check(cudaMemcpyAsync(md_.scalars, mh_.scalars, 16, cudaMemcpyHostToDevice, stream_), "meta");
+  lp_check(cudaStreamSynchronize(stream_), "sync");
+  GemmArgs g;
+  g.N = t_cap;
+  g.n_dev = md_.scalars;
+  g.ws = ws_;
+  g.ws_stride = t_cap;
+  const CUtensorMap* tm = nullptr;
+  const GemmPlan* p = nullptr;
+  const bf16* x = nullptr;
+  switch (which) {
+    case 0: g.M = qkv_out; g.K = h; g.mode = kEpiF32Partial; tm = &w.tm_qkv; p = &sp.qkv; x = x_norm_; break;
+    case 1: g.M = h; g.K = m_.n_q_heads * D; g.mode = kEpiF32Partial; tm = &w.tm_o; p = &sp.o; x = attn_; break;
+    case 2: g.M = 2 * I; g.K = h; g.mode = kEpiSiluMul; g.out = act_; g.ldo = I; tm = &w.tm_gu; p = &sp.gu; x = x_norm_; break;
+    case 3: g.M = h; g.K = I; g.mode = kEpiF32Partial; tm = &w.tm_d; p = &sp.d; x = act_; break;
+    default: throw ShapeMismatch("time_gemm: which in 0..3");
+  }
+  for (int i = 0; i < 2; ++i) gemm(*tm, *p, g, x, t_max_, stream_);  // warm-up
+  lp_check(cudaEventRecord(ev_start_, stream_), "event");
+  for (int i = 0; i < iters; ++i) gemm(*tm, *p, g, x, t_max_, stream_);
+  lp_check(cudaEventRecord(ev_end_, stream_), "event");
+  lp_check(cudaEventSynchronize(ev_end_), "sync");
+  float ms = 0;
+  lp_check(cudaEventElapsedTime(&ms, ev_start_, ev_end_), "elapsed");
+  submitted_ = false;  // lp_wait must not report this timing as a forward
+  return ms / iters;
+}
+
 double Instance::wait() {
   if (!submitted_) throw std::logic_error("lp_wait without a submit");
   lp_check(cudaEventSynchronize(ev_end_), "forward");
@@ -433,6 +508,7 @@ void Instance::read_next_tokens(int32_t* out, int n) {
   std::vector<unsigned long long> keys(n);
   lp_check(cudaMemcpyAsync(keys.data(), next_keys_, size_t(n) * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
   lp_check(cudaStreamSynchronize(stream_), "d2h sync");
+  last_d2h_bytes_ = size_t(n) * 8;
   for (int i = 0; i < n; ++i) out[i] = argmax_token(keys[i]);
 }
 
@@ -570,6 +646,26 @@ int lp_submit(lp_instance* inst, const lp_shape* shape, const lp_member* members
     if (!inst || !shape || !members || !token_ids) throw lp::ConfigError("null argument");
     inst->impl->submit(*shape, members, n, token_ids);
   });
+}
+
+int lp_last_io(lp_instance* inst, int64_t* h2d_bytes, int64_t* d2h_bytes) {
+  return lp::lp_guard([&] {
+    if (h2d_bytes) *h2d_bytes = static_cast<int64_t>(inst->impl->last_h2d_bytes_);
+    if (d2h_bytes) *d2h_bytes = static_cast<int64_t>(inst->impl->last_d2h_bytes_);
+  });
+}
+
+int lp_timer_record(lp_instance* inst, int32_t slot) {
+  return lp::lp_guard([&] { inst->impl->timer_record(slot); });
+}
+
+int lp_timer_elapsed(lp_instance* inst, int32_t slot_a, int32_t slot_b, double* ms) {
+  return lp::lp_guard([&] { *ms = inst->impl->timer_elapsed(slot_a, slot_b); });
+}
+
+int lpk_time_gemm(lp_instance* inst, int32_t layer, int32_t which, int32_t t_cap, int32_t n_live,
+                  int32_t iters, double* avg_ms) {
+  return lp::lp_guard([&] { *avg_ms = inst->impl->time_gemm(layer, which, t_cap, n_live, iters); });
 }
 
 int lp_wait(lp_instance* inst, double* service_ms) {

@@ -49,14 +49,19 @@ struct Meta {
   int* q_len;       // [R]
   int* hist;        // [R]
   int* last_idx;    // [R]
-  int* page_table;  // [R, max_pages]
+  int* page_table;  // flattened page ids of all members (ragged)
+  int* page_off;    // [R] offset of member r in page_table
   int2* work;       // [W]
 };
 
+// Launch plan of one projection at a given token capacity.
+struct GemmPlan {
+  int bn = 16;     // token tile
+  int pair = 1;    // 2 = cta_group::2 CTA pair
+  int splits = 1;  // split-K factor (fp32 partial epilogues only)
+};
 struct SplitPlan {
-  int bn;
-  int s_qkv, s_o, s_d;
-  int bn_lm;
+  GemmPlan qkv, o, gu, d, lm;
 };
 
 class Instance {
@@ -73,6 +78,10 @@ class Instance {
   void session_release(int64_t sid);
   void read_kv(int64_t sid, int layer, int64_t pos0, int64_t n, uint16_t* k, uint16_t* v);
   static void migrate(Instance& src, Instance& dst, int64_t sid);
+  void timer_record(int slot);
+  double timer_elapsed(int a, int b);
+  double time_gemm(int layer, int which, int t_cap, int n_live, int iters);
+  static constexpr int kTimerSlots = 8;
 
   const lp_model_desc& model() const { return m_; }
   int device() const { return d_.device; }
@@ -82,7 +91,8 @@ class Instance {
   void alloc_arena();
   SplitPlan plan_for(int t_cap, int r_cap) const;
   void enqueue_forward(int t_cap, int r_cap, cudaStream_t st);
-  const CUtensorMap& act_map(const bf16* buf, int rows, int cols, int bn);
+  const CUtensorMap& act_map(const bf16* buf, int rows, int cols, int box_rows);
+  void gemm(const CUtensorMap& tm_w, const GemmPlan& p, GemmArgs g, const bf16* x, int x_rows, cudaStream_t st);
   std::vector<int32_t> alloc_pages(int n);
   void ensure_capacity(Session& s, int64_t tokens);
   int64_t graph_key(int64_t l_pad, int depth) const { return l_pad * 1024 + depth; }
@@ -122,9 +132,14 @@ class Instance {
   Meta md_{}, mh_{};
   std::map<std::tuple<const void*, int, int>, CUtensorMap> act_maps_;
 
+  cudaEvent_t timers_[kTimerSlots] = {};
+
   // graphs
   std::map<int64_t, cudaGraphExec_t> graphs_;
   bool submitted_ = false;
+ public:
+  size_t last_h2d_bytes_ = 0, last_d2h_bytes_ = 0;  // host<->device bytes of the last submit / read
+ private:
   int last_n_members_ = 0;
 };
 

@@ -1,4 +1,13 @@
 // tcgen05 GEMM — see gemm_sm100.cuh for the orientation and roles.
+//
+// Two variants of one persistent, warp-specialised kernel:
+//   kPair = 1 : one CTA per 128-row weight tile, tcgen05.mma.cta_group::1.
+//   kPair = 2 : a CTA pair (cluster of 2) per 256-row weight tile,
+//               tcgen05.mma.cta_group::2 issued by the leader CTA. Each CTA
+//               TMA-loads its own 128 weight rows and HALF of the token tile,
+//               so every activation byte crosses L2->SM once per 256 weight
+//               rows (not per 128) and per-SM shared-memory operand traffic
+//               halves. Used for token tiles of >= 128 columns.
 #include <cstdio>
 #include <mutex>
 #include <stdexcept>
@@ -12,16 +21,17 @@ namespace lp {
 
 namespace {
 
-constexpr int kBM = 128;            // weight rows per tile (MMA M)
+constexpr int kBM = 128;            // weight rows per CTA (TMEM lanes)
 constexpr int kBK = 64;             // K per stage: one 128-byte swizzle row of bf16
 constexpr int kThreads = 192;       // warp0 TMA, warp1 MMA, warps2-5 epilogue
 constexpr int kSmemBudget = 196 * 1024;
 constexpr int kEpiStageBytes = 16 * 64 * 2;  // [16 tokens][64 features] bf16
 
-template <int BN>
+template <int BN, int kPair>
 struct Cfg {
+  static constexpr int kBRows = BN / kPair;       // token rows of B held by this CTA
   static constexpr int kABytes = kBM * kBK * 2;   // 16 KiB
-  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (kSmemBudget / kStageBytes) > 8 ? 8 : (kSmemBudget / kStageBytes);
   static constexpr int kTmemCols = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
@@ -33,11 +43,11 @@ __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x));
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-template <int BN>
+template <int BN, int kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, kPair>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -52,15 +62,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t rank = kPair == 2 ? cluster_rank() : 0;
+  const bool leader = rank == 0;
   pdl_trigger();
 
   // n_dev is written by the pre-graph H2D copy, never by a kernel: safe before pdl_wait.
   const int n_live = args.n_dev ? min(*args.n_dev, args.N) : args.N;
-  const int m_tiles = args.M / kBM;
+  const int m_tiles = args.M / (kBM * kPair);   // tiles of this variant (128 or 256 rows)
   const int n_tiles = (args.N + BN - 1) / BN;
   const int num_kb = args.K / kBK;
   const int splits = args.splits;
   const int units = splits * m_tiles * n_tiles;
+  const int worker = blockIdx.x / kPair;        // CTA (pair) index
+  const int n_workers = gridDim.x / kPair;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -71,13 +85,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4 * kPair);  // every epilogue warp of the pair
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (kPair == 2) tmem_alloc_pair<C::kTmemCols>(tmem_slot);
+    else tmem_alloc<C::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair == 2) cluster_sync();  // peer barriers initialised before remote use
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -86,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int rest = w / n_tiles;
     const int m = rest % m_tiles;
     s = rest / m_tiles;
-    m0 = m * kBM;
+    m0 = m * kBM * kPair + static_cast<int>(rank) * kBM;  // this CTA's 128 weight rows
     n0 = n * BN;
     const int base = num_kb / splits, rem = num_kb % splits;
     kb0 = s * base + min(s, rem);
@@ -98,85 +116,107 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_first();  // weights stream once
       const uint64_t pol_x = policy_evict_last();   // activations are re-read per m tile
+      const uint32_t bar0 = kPair == 2 ? mapa(smem_u32(&full[0]), 0) : smem_u32(&full[0]);
+      auto load = [&](int stage, int kb, int m0, int n0, bool a_part, bool b_part) {
+        const uint32_t bar = bar0 + stage * 8;
+        if constexpr (kPair == 2) {
+          if (a_part) tma_load_2d_pair(sA + stage * C::kABytes, &tmA, bar, kb * kBK, m0, pol_w);
+          if (b_part)
+            tma_load_2d_pair(sB + stage * C::kBBytes, &tmB, bar, kb * kBK,
+                             n0 + static_cast<int>(rank) * C::kBRows, pol_x);
+        } else {
+          if (a_part) tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * kBK, m0, pol_w);
+          if (b_part) tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * kBK, n0, pol_x);
+        }
+      };
+      // The leader's full barrier expects the bytes of the whole pair.
+      auto expect = [&](int stage) {
+        if (leader) mbar_arrive_expect_tx(&full[stage], C::kStageBytes * kPair);
+      };
       // Weight tiles do not depend on the previous kernel: fill the pipeline
       // with them before waiting on it (PDL), then add the activation tiles.
       int pre = 0;
-      int pre_w = -1, pre_kb0 = 0, pre_m0 = 0, pre_n0 = 0;
-      for (int w = blockIdx.x; w < units; w += gridDim.x) {
+      int pre_w = -1, pre_kb0 = 0, pre_n0 = 0;
+      for (int w = worker; w < units; w += n_workers) {
         int s, m0, n0, kb0, kb1;
         decode(w, s, m0, n0, kb0, kb1);
         if (n0 >= n_live) continue;
-        pre_w = w; pre_kb0 = kb0; pre_m0 = m0; pre_n0 = n0;
+        pre_w = w; pre_kb0 = kb0; pre_n0 = n0;
         pre = min(kb1 - kb0, C::kStages);
         for (int i = 0; i < pre; ++i) {
-          mbar_arrive_expect_tx(&full[i], C::kStageBytes);
-          tma_load_2d(sA + i * C::kABytes, &tmA, &full[i], (kb0 + i) * kBK, m0, pol_w);
+          expect(i);
+          load(i, kb0 + i, m0, n0, true, false);
         }
         break;
       }
       pdl_wait();
-      for (int i = 0; i < pre; ++i)
-        tma_load_2d(sB + i * C::kBBytes, &tmB, &full[i], (pre_kb0 + i) * kBK, pre_n0, pol_x);
-      (void)pre_m0;
+      for (int i = 0; i < pre; ++i) load(i, pre_kb0 + i, 0, pre_n0, false, true);
       int stage = pre % C::kStages;
       uint32_t phase = pre == C::kStages ? 1u : 0u;
-      for (int w = (pre_w >= 0 ? pre_w : units); w < units; w += gridDim.x) {
+      for (int w = (pre_w >= 0 ? pre_w : units); w < units; w += n_workers) {
         int s, m0, n0, kb0, kb1;
         decode(w, s, m0, n0, kb0, kb1);
         if (n0 >= n_live) continue;
         for (int kb = (w == pre_w ? kb0 + pre : kb0); kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-          tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * kBK, m0, pol_w);
-          tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * kBK, n0, pol_x);
+          expect(stage);
+          load(stage, kb, m0, n0, true, true);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ----------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc = idesc_bf16(kBM, BN);
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t aphase = 0;
-    for (int w = blockIdx.x; w < units; w += gridDim.x) {
-      int s, m0, n0, kb0, kb1;
-      decode(w, s, m0, n0, kb0, kb1);
-      if (n0 >= n_live) continue;
-      mbar_wait(&tempty[acc], aphase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
+    // ----------------------------------------------------------- MMA issuer (leader of a pair)
+    if (leader) {
+      constexpr uint32_t idesc = idesc_bf16(kBM * kPair, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int w = worker; w < units; w += n_workers) {
+        int s, m0, n0, kb0, kb1;
+        decode(w, s, m0, n0, kb0, kb1);
+        if (n0 >= n_live) continue;
+        mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint64_t a_desc = sdesc_sw128(smem_u32(sA + stage * C::kABytes));
-          const uint64_t b_desc = sdesc_sw128(smem_u32(sB + stage * C::kBBytes));
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t a_desc = sdesc_sw128(smem_u32(sA + stage * C::kABytes));
+            const uint64_t b_desc = sdesc_sw128(smem_u32(sB + stage * C::kBBytes));
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            // +32 bytes per UMMA_K=16 slice inside the swizzle atom (>>4 => +2).
-            tc_mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc,
-                        (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < kBK / 16; ++k) {
+              // +32 bytes per UMMA_K=16 slice inside the swizzle atom (>>4 => +2).
+              const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
+              if constexpr (kPair == 2) tc_mma_bf16_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, accum);
+              else tc_mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, accum);
+            }
+            if constexpr (kPair == 2) tc_commit_pair(&empty[stage]);
+            else tc_commit(&empty[stage]);
           }
-          tc_commit(&empty[stage]);
+          __syncwarp();
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+        if (elect_one()) {
+          if constexpr (kPair == 2) tc_commit_pair(&tfull[acc]);
+          else tc_commit(&tfull[acc]);
         }
         __syncwarp();
-        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
       }
-      if (elect_one()) tc_commit(&tfull[acc]);
-      __syncwarp();
-      if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
   } else {
     // ----------------------------------------------------------- epilogue
     const int q = warp % 4;          // TMEM lane quarter this warp may touch
     const int row = q * 32 + lane;   // tile row == TMEM lane
     const int et = threadIdx.x - 64; // 0..127 within the epilogue group
+    const uint32_t tempty_leader = kPair == 2 ? mapa(smem_u32(&tempty[0]), 0) : 0;
     int acc = 0;
     uint32_t aphase = 0;
     int sbuf = 0;
-    for (int w = blockIdx.x; w < units; w += gridDim.x) {
+    for (int w = worker; w < units; w += n_workers) {
       int s, m0, n0, kb0, kb1;
       decode(w, s, m0, n0, kb0, kb1);
       if (n0 >= n_live) continue;
@@ -239,16 +279,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (kPair == 2) mbar_arrive_remote(tempty_leader + acc * 8);
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair == 2) cluster_sync();  // the peer may still signal our barriers
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<C::kTmemCols>(tmem_base);
+    if constexpr (kPair == 2) tmem_dealloc_pair<C::kTmemCols>(tmem_base);
+    else tmem_dealloc<C::kTmemCols>(tmem_base);
   }
 }
 
@@ -272,21 +317,40 @@ EncodeFn get_encode() {
   return fn;
 }
 
-template <int BN>
+template <int BN, int kPair>
 void launch_bn(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                cudaStream_t stream, int max_ctas) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, kPair>;
   static bool attr_set = false;
+  auto* kern = gemm_bf16_tn_kernel<BN, kPair>;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::kSmem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr_set = true;
   }
-  const int units = a.splits * (a.M / kBM) * ((a.N + BN - 1) / BN);
-  int grid = num_sms();
-  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  const int units = a.splits * (a.M / (kBM * kPair)) * ((a.N + BN - 1) / BN);
+  int grid = num_sms() / kPair;
+  if (max_ctas > 0 && max_ctas / kPair < grid) grid = max_ctas / kPair;
   if (units < grid) grid = units;
-  launch_k(gemm_bf16_tn_kernel<BN>, dim3(grid), dim3(kThreads), C::kSmem, stream, tmA, tmB, a);
+  grid *= kPair;
+  if constexpr (kPair == 1) {
+    launch_k(kern, dim3(grid), dim3(kThreads), C::kSmem, stream, tmA, tmB, a);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, kern, tmA, tmB, a);
+  }
 }
 
 }  // namespace
@@ -318,19 +382,31 @@ CUtensorMap make_tmap_bf16(const void* ptr, uint64_t rows, uint64_t cols, uint32
   return m;
 }
 
+int gemm_b_box_rows(int bn, int pair) { return bn / pair; }
+
 void gemm_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, int bn,
-                 cudaStream_t stream, int max_ctas) {
-  if (a.M % kBM != 0 || a.K % kBK != 0 || a.N < 1 || a.splits < 1) {
+                 cudaStream_t stream, int max_ctas, int pair) {
+  if (a.M % (kBM * pair) != 0 || a.K % kBK != 0 || a.N < 1 || a.splits < 1) {
     throw std::runtime_error("gemm_launch: unsupported shape M=" + std::to_string(a.M) +
-                             " K=" + std::to_string(a.K) + " N=" + std::to_string(a.N));
+                             " K=" + std::to_string(a.K) + " N=" + std::to_string(a.N) +
+                             " pair=" + std::to_string(pair));
   }
   if (a.mode == kEpiSiluMul && (a.ldo % 8 != 0)) throw std::runtime_error("gemm_launch: SiLU ldo % 8");
+  if (pair == 2) {
+    switch (bn) {
+      case 32: launch_bn<32, 2>(tmA, tmB, a, stream, max_ctas); return;
+      case 64: launch_bn<64, 2>(tmA, tmB, a, stream, max_ctas); return;
+      case 128: launch_bn<128, 2>(tmA, tmB, a, stream, max_ctas); return;
+      case 256: launch_bn<256, 2>(tmA, tmB, a, stream, max_ctas); return;
+      default: throw std::runtime_error("gemm_launch: bad paired bn " + std::to_string(bn));
+    }
+  }
   switch (bn) {
-    case 16: launch_bn<16>(tmA, tmB, a, stream, max_ctas); break;
-    case 32: launch_bn<32>(tmA, tmB, a, stream, max_ctas); break;
-    case 64: launch_bn<64>(tmA, tmB, a, stream, max_ctas); break;
-    case 128: launch_bn<128>(tmA, tmB, a, stream, max_ctas); break;
-    case 256: launch_bn<256>(tmA, tmB, a, stream, max_ctas); break;
+    case 16: launch_bn<16, 1>(tmA, tmB, a, stream, max_ctas); break;
+    case 32: launch_bn<32, 1>(tmA, tmB, a, stream, max_ctas); break;
+    case 64: launch_bn<64, 1>(tmA, tmB, a, stream, max_ctas); break;
+    case 128: launch_bn<128, 1>(tmA, tmB, a, stream, max_ctas); break;
+    case 256: launch_bn<256, 1>(tmA, tmB, a, stream, max_ctas); break;
     default: throw std::runtime_error("gemm_launch: bad bn " + std::to_string(bn));
   }
 }

@@ -43,10 +43,13 @@ struct GemmArgs {
 // [box_rows, 64 cols], 128-byte swizzle.
 CUtensorMap make_tmap_bf16(const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
 
-// Launch. `bn` is the token-tile width (16, 32, 64, 128 or 256); tmB must have
-// been built with box_rows == bn.
+// Launch. `bn` is the token-tile width (16, 32, 64, 128 or 256). pair = 2
+// selects the CTA-pair (cta_group::2, M = 256 per pair) variant; M must then
+// be a multiple of 256 and bn >= 32. tmB must have been built with
+// box_rows == gemm_b_box_rows(bn, pair) (= bn / pair).
 void gemm_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, int bn,
-                 cudaStream_t stream, int max_ctas = 0);
+                 cudaStream_t stream, int max_ctas = 0, int pair = 1);
+int gemm_b_box_rows(int bn, int pair);
 
 int num_sms();
 

@@ -173,6 +173,27 @@ class PrefillInstance:
         _check(N.lib().lp_read_kv(self._h, session_id, layer, pos0, n, k.ctypes.data, v.ctypes.data))
         return k, v
 
+    def last_io(self) -> tuple[int, int]:
+        """(H2D bytes of the last submit, D2H bytes of the last first-token read)."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(N.lib().lp_last_io(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def timer_record(self, slot: int) -> None:
+        _check(N.lib().lp_timer_record(self._h, slot))
+
+    def timer_elapsed(self, a: int, b: int) -> float:
+        ms = ctypes.c_double()
+        _check(N.lib().lp_timer_elapsed(self._h, a, b, ctypes.byref(ms)))
+        return ms.value
+
+    def time_gemm(self, layer: int, which: int, t_cap: int, n_live: int, iters: int = 20) -> float:
+        """Average ms of one projection GEMM (0 qkv, 1 o, 2 gate/up, 3 down)
+        with this instance's weights and launch plan (CUDA events)."""
+        ms = ctypes.c_double()
+        _check(N.lib().lpk_time_gemm(self._h, layer, which, t_cap, n_live, iters, ctypes.byref(ms)))
+        return ms.value
+
     @staticmethod
     def migrate(src: "PrefillInstance", dst: "PrefillInstance", session_id: int) -> None:
         _check(N.lib().lp_session_migrate(src._h, dst._h, session_id))

@@ -15,7 +15,7 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def run_gemm(M, Ntok, K, splits=1, mode=0, bn=None, bias=False, n_live=None, seed=0):
+def run_gemm(M, Ntok, K, splits=1, mode=0, bn=None, bias=False, n_live=None, seed=0, pair=1):
     g = torch.Generator(device="cuda").manual_seed(seed)
     W = (torch.randn(M, K, device="cuda", generator=g) * 0.05).bfloat16()
     X = torch.randn(Ntok, K, device="cuda", generator=g).bfloat16()
@@ -43,7 +43,7 @@ def run_gemm(M, Ntok, K, splits=1, mode=0, bn=None, bias=False, n_live=None, see
         ldo = M
     rc = N.lib().lpk_gemm(_ptr(W), _ptr(X), _ptr(out) if out is not None else None,
                           _ptr(ws) if ws is not None else None, _ptr(b) if b is not None else None,
-                          M, Ntok, K, splits, mode, bn, ldo, _ptr(nd) if nd is not None else None, None)
+                          M, Ntok, K, splits, mode, bn, ldo, _ptr(nd) if nd is not None else None, None, pair)
     N.check(rc)
     torch.cuda.synchronize()
     if mode == 1:
@@ -87,3 +87,17 @@ def test_gemm_f32_and_live_count():
     got, ref = run_gemm(1024, 256, 512, mode=3, n_live=77)
     _close(got, ref, n_live=77)
     assert torch.all(got[80:] == 0)
+
+
+@pytest.mark.parametrize("M,Ntok,K,bn,mode,splits", [(256, 128, 512, 128, 0, 1), (512, 256, 1024, 256, 0, 1),
+                                                      (3584, 300, 3584, 256, 1, 3), (1536, 200, 256, 256, 2, 1),
+                                                      (4608, 64, 3584, 64, 1, 4), (1024, 1000, 512, 128, 3, 1)])
+def test_gemm_pair(M, Ntok, K, bn, mode, splits):
+    """cta_group::2 variant (CTA pair, M = 256 per pair, B split over the pair)."""
+    got, ref = run_gemm(M, Ntok, K, splits=splits, mode=mode, bn=bn, pair=2, bias=(mode == 0))
+    _close(got, ref)
+
+
+def test_gemm_pair_live_count():
+    got, ref = run_gemm(1024, 512, 512, mode=3, bn=256, pair=2, n_live=300)
+    _close(got, ref, n_live=300)
