@@ -54,6 +54,8 @@ LAMBDA_PER_MS = 1.0      # saturating offered load per GPU (dispatch sequence fo
 DURATION_MS = 4000
 LAMBDA_TTFT = 0.25       # sub-saturation load for the reported TTFT p50/p90
 DURATION_TTFT_MS = 4000
+if os.environ.get("LP_BENCH_QUICK") == "1":  # profiling runs: same phases, short live streams
+    DURATION_MS, DURATION_TTFT_MS = 600, 600
 TOKEN_SEED = 7
 
 
@@ -64,6 +66,19 @@ def load_peaks() -> dict:
         return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
                 "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "src": "measured"}
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
+
+
+def committed_traffic(t_cap: int):
+    """DRAM bytes per launch of the dominant kernel from the committed
+    `ncu --set full` capture (profiles/r01_dominant_kernel.json), if it was
+    taken at this step capacity; else None."""
+    p = ROOT / "profiles" / "r01_dominant_kernel.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    if d.get("t_cap") != t_cap:
+        return None
+    return d.get("dram_bytes_per_launch")
 
 
 class ClockSampler:
@@ -127,22 +142,32 @@ def dist_init(ws: int, local: int):
     return dist
 
 
-def dist_max(dist, x: float, local: int) -> float:
+def _reduce(dist, x: float, local: int, op) -> float:
     if dist is None:
         return x
     import torch
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{local}"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=op)
     return float(t.item())
+
+
+def dist_max(dist, x: float, local: int) -> float:
+    """Timed region of a multi-GPU run = max over ranks (device time)."""
+    return _reduce(dist, x, local, dist.ReduceOp.MAX if dist is not None else None)
 
 
 def dist_sum(dist, x: float, local: int) -> float:
-    if dist is None:
-        return x
-    import torch
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    """Whole-job work = sum over ranks (requests processed)."""
+    return _reduce(dist, x, local, dist.ReduceOp.SUM if dist is not None else None)
+
+
+def aggregate_throughput(dist, reqs: int, dev_ms: float, local: int) -> tuple[float, float, float]:
+    """(whole-job req/s, total requests, max-over-ranks ms) for independent
+    instances: the job finishes when the slowest rank does."""
+    t_max = dist_max(dist, dev_ms, local)
+    reqs_all = dist_sum(dist, float(reqs), local)
+    return reqs_all / (t_max / 1000.0), reqs_all, t_max
 
 
 def barrier(dist):
@@ -332,6 +357,8 @@ def run_ours(args) -> None:
             inst.release(m[1] + uniq * (i + 1))
     barrier(dist)
     reqs = 0
+    import torch
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ selects this region
     with ClockSampler(local) as clk:
         inst.timer_record(0)
         for j in range(args.steps):
@@ -343,10 +370,9 @@ def run_ours(args) -> None:
             reqs += len(ms)
         inst.timer_record(1)
         dev_ms = inst.timer_elapsed(0, 1)
+    torch.cuda.nvtx.range_pop()
     barrier(dist)
-    t_max = dist_max(dist, dev_ms, local)
-    reqs_all = dist_sum(dist, reqs, local)
-    value = reqs_all / (t_max / 1000.0)
+    value, reqs_all, t_max = aggregate_throughput(dist, reqs, dev_ms, local)
 
     # ---- Phase C: end to end through the C ABI with host buffers
     barrier(dist)
@@ -404,7 +430,7 @@ def run_ours(args) -> None:
                                "ttft_p90_ms": st.ttft_p90_ms},
             "roofline": {"kernel": "gemm_bf16_tn_kernel gate/up (+SiLU*up)", "bound": "hbm" if hbm_bound else "tensor",
                          "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-                         "traffic": None, "t_cap": t_cap, "n_live": n_live, "avg_ms": gu_ms,
+                         "traffic": committed_traffic(t_cap), "t_cap": t_cap, "n_live": n_live, "avg_ms": gu_ms,
                          "peak_src": peaks["src"],
                          "forward_hbm_gbs": fw_bytes / (t_max * 1e-3) / 1e9 / (1 if ws == 1 else ws),
                          "forward_tflops": fw_flops / (t_max * 1e-3) / 1e12 / (1 if ws == 1 else ws)},

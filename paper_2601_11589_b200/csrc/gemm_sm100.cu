@@ -116,7 +116,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ----------------------------------------------------------- TMA producer
     if (elect_one()) {
-      const uint64_t pol_w = policy_evict_first();  // weights stream once
+      // A weight tile with a single consumer streams once (evict first); with
+      // several token tiles its sibling units (consecutive unit ids, resident
+      // at the same time) re-read it from L2, so keep normal priority.
+      const uint64_t pol_w = n_tiles > 1 ? policy_evict_normal() : policy_evict_first();
       const uint64_t pol_x = policy_evict_last();   // activations are re-read per m tile
       const uint32_t bar0 = kPair == 2 ? mapa(smem_u32(&full[0]), 0) : smem_u32(&full[0]);
       auto load = [&](int stage, int kb, int m0, int n0, bool a_part, bool b_part) {
