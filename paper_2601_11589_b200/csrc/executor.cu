@@ -47,8 +47,20 @@ GemmPlan plan_gemm(int M, int K, int t_cap, bool allow_split, int sms) {
   p.pair = (p.bn >= 128 && M % 256 == 0) ? 2 : 1;
   const int workers = sms / p.pair;
   const int units = (M / (128 * p.pair)) * ((t_cap + p.bn - 1) / p.bn);
-  if (allow_split && units < workers) {
-    p.splits = std::max(1, std::min({workers / units, std::max(1, (K / 64) / 4), 8}));
+  if (!allow_split) return p;
+  // Split-K factor minimising wave quantisation: time ~ ceil(units*S/workers)/S
+  // per unit of work, with a small charge per extra split for the fp32
+  // partial round trip; at least 4 k-blocks per split, and S*T bounded so the
+  // partials stay a small fraction of the weight stream.
+  const int s_max = std::max(1, std::min({8, (K / 64) / 4, std::max(1, 4096 / t_cap)}));
+  double best = 1e30;
+  for (int s = 1; s <= s_max; ++s) {
+    const double waves = static_cast<double>((units * s + workers - 1) / workers);
+    const double cost = waves / s * (1.0 + 0.03 * (s - 1));
+    if (cost < best - 1e-9) {
+      best = cost;
+      p.splits = s;
+    }
   }
   return p;
 }

@@ -116,6 +116,11 @@ class PrefillInstance:
             self._h = ctypes.c_void_p()
 
     def __del__(self):
+        # Never touch the CUDA runtime while the interpreter is finalising (its
+        # own teardown may already be in progress); the process exit frees it.
+        import sys
+        if sys.is_finalizing():
+            return
         try:
             self.close()
         except Exception:

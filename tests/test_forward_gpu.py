@@ -71,7 +71,8 @@ def tiny():
     inst = PrefillInstance(TINY, max_tokens=4096, max_members=64, kv_pages=512)
     inst.capture_graphs(lengths=(8, 16, 32, 64, 128, 256), depths=(1, 2, 4, 8))
     oracle = FO.OracleModel(FO.TINY)
-    return inst, oracle, PageOracle(512)
+    yield inst, oracle, PageOracle(512)
+    inst.close()
 
 
 def test_tiny_scenario(tiny):
@@ -119,3 +120,26 @@ def test_7b_shaped_two_layers():
     _compare(inst, oracle, pages, 600, 1, KIND_STANDARD, [M(3, 2, 600, 0)], tol=tol)
     # layer >= 1 inherits the residual-stream noise floor: <= 4 bf16 ulps at |x| < 4
     _kv_check(inst, oracle, 0, [0, 1], max_abs=6.25e-2, mean_abs=5e-3)
+    inst.close()
+
+
+def test_session_migration_between_instances():
+    """Spatial disaggregation: a re-prefill lands on another instance; the
+    session's KV pages move (lp_session_migrate; P2P over NVLink across
+    devices, device copy here) and the forward matches the oracle."""
+    src = PrefillInstance(TINY, max_tokens=1024, max_members=8, kv_pages=64)
+    dst = PrefillInstance(TINY, max_tokens=1024, max_members=8, kv_pages=64)
+    oracle = FO.OracleModel(FO.TINY)
+    p_src, p_dst = PageOracle(64), PageOracle(64)
+    # occupy a few pages on dst so the migrated session gets different page ids
+    _compare(dst, oracle, p_dst, 0, 0, KIND_PACKED, [Member(0, 50, 100, 0)])
+    _compare(src, oracle, p_src, 0, 0, KIND_PACKED, [Member(1, 7, 150, 0)])
+    PrefillInstance.migrate(src, dst, 7)
+    assert src.session_pages(7) == ([], 0)
+    pages, kv = dst.session_pages(7)
+    assert kv == 150 and pages == [2, 3, 4]
+    p_dst.submit([(7, 150, 0)])  # the oracle allocator sees the import as an allocation
+    _kv_check(dst, oracle, 7, [0, 1])
+    _compare(dst, oracle, p_dst, 0, 0, KIND_PACKED, [Member(2, 7, 40, 150)])
+    src.close()
+    dst.close()
