@@ -1,5 +1,6 @@
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <tuple>
@@ -77,6 +78,7 @@ Instance::Instance(const lp_model_desc& m, const lp_instance_desc& d) : m_(m), d
   d_.page_size = kPage;
   if (d_.max_tokens <= 0) d_.max_tokens = 16384;
   if (d_.max_members <= 0) d_.max_members = 64;
+  if (const char* e = std::getenv("LP_FUSE_EPI"); e && e[0] == '0') fuse_epilogues_ = false;
   lp_check(cudaSetDevice(d.device), "cudaSetDevice");
   lp_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   lp_check(cudaEventCreate(&ev_start_), "event");
@@ -273,10 +275,18 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st) {
     GemmArgs g;
     g.M = qkv_out; g.N = t_cap; g.K = h; g.n_dev = n_tok;
     g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
-    gemm(w.tm_qkv, p.qkv, g, x_norm_, t_max_, st);
-    QkvCtx qc{n_tok, t_cap, nq, nkv, D, kPage, ws_, p.qkv.splits, size_t(t_cap), w.bqkv,
-              md_.positions, md_.slots, inv_freq_, q_, kv_layer};
-    qkv_post(qc, st);
+    if (fuse_epilogues_ && p.qkv.splits == 1 && D == 128) {
+      // Bias + RoPE + q / paged-KV writes straight from TMEM (no fp32 round trip).
+      g.mode = kEpiQkvRope;
+      g.bias = w.bqkv;
+      g.qkv = QkvEpi{md_.positions, md_.slots, inv_freq_, q_, kv_layer, nq, nkv, kPage};
+      gemm(w.tm_qkv, p.qkv, g, x_norm_, t_max_, st);
+    } else {
+      gemm(w.tm_qkv, p.qkv, g, x_norm_, t_max_, st);
+      QkvCtx qc{n_tok, t_cap, nq, nkv, D, kPage, ws_, p.qkv.splits, size_t(t_cap), w.bqkv,
+                md_.positions, md_.slots, inv_freq_, q_, kv_layer};
+      qkv_post(qc, st);
+    }
     AttnCtx ac{md_.scalars + 2, md_.work, md_.q_start, md_.q_len, md_.hist, md_.page_table,
                md_.page_off, q_, kv_layer, attn_, nq, nkv,
                static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)))};
@@ -285,8 +295,13 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st) {
     g = GemmArgs{};
     g.M = h; g.N = t_cap; g.K = nq * D; g.n_dev = n_tok;
     g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
+    const bool o_fused = fuse_epilogues_ && p.o.splits == 1;
+    if (o_fused) {  // residual add in the epilogue; the norm kernel then reads x_resid only
+      g.mode = kEpiResidAdd;
+      g.resid = x_resid_;
+    }
     gemm(w.tm_o, p.o, g, attn_, t_max_, st);
-    resid_rmsnorm(rc, ws_, p.o.splits, t_cap, x_resid_, w.g_mlp, x_norm_, st);
+    resid_rmsnorm(rc, ws_, o_fused ? 0 : p.o.splits, t_cap, x_resid_, w.g_mlp, x_norm_, st);
     // gate/up with fused SiLU*up.
     g = GemmArgs{};
     g.M = 2 * I; g.N = t_cap; g.K = h; g.n_dev = n_tok;
@@ -296,9 +311,14 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st) {
     g = GemmArgs{};
     g.M = h; g.N = t_cap; g.K = I; g.n_dev = n_tok;
     g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
+    const bool d_fused = fuse_epilogues_ && p.d.splits == 1;
+    if (d_fused) {
+      g.mode = kEpiResidAdd;
+      g.resid = x_resid_;
+    }
     gemm(w.tm_d, p.d, g, act_, t_max_, st);
     const bf16* g_next = (l + 1 < m_.layers) ? layers_[l + 1].g_attn : g_final_;
-    resid_rmsnorm(rc, ws_, p.d.splits, t_cap, x_resid_, g_next, x_norm_, st);
+    resid_rmsnorm(rc, ws_, d_fused ? 0 : p.d.splits, t_cap, x_resid_, g_next, x_norm_, st);
   }
   // Final norm already applied; LM head on the last real token per member.
   gather_rows(n_mem, r_cap, md_.last_idx, x_norm_, x_last_, h, next_keys_, st);
@@ -496,6 +516,10 @@ double Instance::time_gemm(int layer, int which, int t_cap, int n_live, int iter
     case 3: g.M = h; g.K = I; g.mode = kEpiF32Partial; tm = &w.tm_d; p = &sp.d; x = act_; break;
     default: throw ShapeMismatch("time_gemm: which in 0..3");
   }
+  // Realistic operand values (unit-variance activations): an all-zero input
+  // would under-state power draw and over-state the clock.
+  init_weights(const_cast<bf16*>(x), size_t(t_cap) * g.K, 77, 999, std::sqrt(3.0f) / 8388608.0f, 0, g.K,
+               stream_);
   for (int i = 0; i < 2; ++i) gemm(*tm, *p, g, x, t_max_, stream_);  // warm-up
   lp_check(cudaEventRecord(ev_start_, stream_), "event");
   for (int i = 0; i < iters; ++i) gemm(*tm, *p, g, x, t_max_, stream_);

@@ -133,6 +133,9 @@ class Instance {
   std::map<std::tuple<const void*, int, int>, CUtensorMap> act_maps_;
 
   cudaEvent_t timers_[kTimerSlots] = {};
+  // Fused GEMM epilogues (QKV bias+RoPE+KV append, residual add) when the
+  // plan has no split-K; LP_FUSE_EPI=0 disables them (A/B measurements).
+  bool fuse_epilogues_ = true;
 
   // graphs
   std::map<int64_t, cudaGraphExec_t> graphs_;

@@ -25,7 +25,9 @@ constexpr int kBM = 128;            // weight rows per CTA (TMEM lanes)
 constexpr int kBK = 64;             // K per stage: one 128-byte swizzle row of bf16
 constexpr int kThreads = 192;       // warp0 TMA, warp1 MMA, warps2-5 epilogue
 constexpr int kSmemBudget = 196 * 1024;
-constexpr int kEpiStageBytes = 16 * 64 * 2;  // [16 tokens][64 features] bf16
+// Epilogue staging, double-buffered: SiLU uses [16 tokens][64 features] bf16,
+// the fused QKV/RoPE epilogue [128 rows][17] fp32 (padded: conflict-free).
+constexpr int kEpiStageBytes = 128 * 17 * 4;
 
 template <int BN, int kPair>
 struct Cfg {
@@ -271,6 +273,68 @@ __global__ void __launch_bounds__(kThreads, 1)
             *reinterpret_cast<uint4*>(dst) = val;
           }
           sbuf ^= 1;
+        } else if (args.mode == kEpiResidAdd) {
+          // All 16 residual loads are issued before the first store: the
+          // compiler cannot reorder a load above a possibly-aliasing store.
+          float* dst = args.resid + static_cast<size_t>(nbase) * args.M + m;
+          float r[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) r[j] = j < cnt ? dst[static_cast<size_t>(j) * args.M] : 0.f;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < cnt) dst[static_cast<size_t>(j) * args.M] = r[j] + v[j];
+        } else if (args.mode == kEpiQkvRope) {
+          // This CTA's 128 rows are one head (head_dim 128): bias, then RoPE
+          // for q/k heads (rotate-half pairs (i, i+64) live in warps q and
+          // q^2: exchanged through smem), then bf16 out to q or the KV page.
+          const QkvEpi& e = args.qkv;
+          const int hd = m0 >> 7;
+          const float b = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(args.bias)[m]);
+          // Per-token metadata into registers before any store (see ResidAdd).
+          int pos[16], slot[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            pos[j] = j < cnt ? e.positions[nbase + j] : 0;
+            slot[j] = j < cnt ? e.slots[nbase + j] : 0;
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += b;
+          if (hd < e.nq + e.nkv) {  // uniform per CTA
+            float* xs = reinterpret_cast<float*>(epi_stage) + sbuf * (128 * 17);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) xs[row * 17 + j] = v[j];
+            epi_bar();
+            const int prow = row ^ 64;
+            const float f = e.inv_freq[row & 63];
+            const float sgn = row < 64 ? -1.f : 1.f;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float p = xs[prow * 17 + j];
+              float sn, cs;
+              sincosf(static_cast<float>(pos[j]) * f, &sn, &cs);
+              v[j] = v[j] * cs + sgn * p * sn;
+            }
+            sbuf ^= 1;
+          }
+          if (hd < e.nq) {
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(e.q_out) + static_cast<size_t>(nbase) * e.nq * 128 + m;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < cnt) dst[static_cast<size_t>(j) * e.nq * 128] = __float2bfloat16_rn(v[j]);
+          } else {
+            const bool is_v = hd >= e.nq + e.nkv;
+            const int g = is_v ? hd - e.nq - e.nkv : hd - e.nq;
+            const size_t page_elems = static_cast<size_t>(2) * e.nkv * e.page_size * 128;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (j < cnt) {
+                const int page = slot[j] / e.page_size, s_in = slot[j] % e.page_size;
+                __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(e.kv_layer) + page * page_elems +
+                                     ((static_cast<size_t>(is_v ? 1 : 0) * e.nkv + g) * e.page_size + s_in) * 128 + row;
+                *dst = __float2bfloat16_rn(v[j]);
+              }
+            }
+          }
         } else if (args.mode == kEpiBf16) {
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) +
                                static_cast<size_t>(nbase) * args.ldo + m;

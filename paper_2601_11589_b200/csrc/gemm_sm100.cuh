@@ -23,6 +23,19 @@ enum GemmEpilogue : int {
   kEpiF32Partial = 1,  // ws[(split*ws_stride + n)*M + m] = acc
   kEpiSiluMul = 2,     // rows interleaved (gate,up): out_bf16[n*ldo + m/2] = silu(g)*u
   kEpiF32 = 3,         // out_f32[n*ldo + m] = acc
+  kEpiQkvRope = 4,     // q/k/v = bf16(RoPE(acc + bias)): q -> q_out, k/v -> paged KV slot (split-K = 1)
+  kEpiResidAdd = 5,    // resid_f32[n*M + m] += acc (split-K = 1)
+};
+
+// Extra operands of the fused QKV epilogue (kEpiQkvRope). head_dim == 128:
+// one 128-row weight tile is exactly one head.
+struct QkvEpi {
+  const int* positions = nullptr;  // [T] absolute positions
+  const int* slots = nullptr;      // [T] page * page_size + slot
+  const float* inv_freq = nullptr; // [64]
+  void* q_out = nullptr;           // bf16 [T, nq*128]
+  void* kv_layer = nullptr;        // bf16 paged cache of this layer
+  int nq = 0, nkv = 0, page_size = 64;
 };
 
 struct GemmArgs {
@@ -37,6 +50,8 @@ struct GemmArgs {
   const void* bias = nullptr;  // bf16[M] (kEpiBf16 only)
   float* ws = nullptr;
   int ws_stride = 0;    // rows per split slice in ws (>= N)
+  float* resid = nullptr;  // kEpiResidAdd target [N, M] fp32
+  QkvEpi qkv;              // kEpiQkvRope operands
 };
 
 // Build a 2D bf16 tensor map over a row-major [rows, cols] matrix, box

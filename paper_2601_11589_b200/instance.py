@@ -13,6 +13,7 @@ than `depth` (cost_model.cpp:131-139), `ConfigError` for bad descriptors.
 from __future__ import annotations
 
 import ctypes
+import sys as _sys
 from dataclasses import dataclass
 
 import numpy as np
@@ -118,8 +119,7 @@ class PrefillInstance:
     def __del__(self):
         # Never touch the CUDA runtime while the interpreter is finalising (its
         # own teardown may already be in progress); the process exit frees it.
-        import sys
-        if sys.is_finalizing():
+        if _sys.is_finalizing():
             return
         try:
             self.close()

@@ -143,3 +143,25 @@ def test_session_migration_between_instances():
     _compare(dst, oracle, p_dst, 0, 0, KIND_PACKED, [Member(2, 7, 40, 150)])
     src.close()
     dst.close()
+
+
+def test_fused_epilogues_match_unfused(monkeypatch):
+    """At 4096 tokens the launch plan has no split-K, so QKV runs the fused
+    bias+RoPE+KV-append epilogue and O/down the fused residual add; the
+    result must match the unfused path (LP_FUSE_EPI=0) and the oracle."""
+    from paper_2601_11589_b200.instance import QWEN25_7B
+    cfg = QWEN25_7B.with_layers(2)
+    members = [Member(i, 300 + i, 256, 0) for i in range(16)]
+    toks = _toks(members, cfg.vocab)
+    logits = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("LP_FUSE_EPI", fuse)
+        inst = PrefillInstance(cfg, max_tokens=4096, max_members=16, kv_pages=128, use_graphs=False)
+        inst.forward(0, 0, KIND_PACKED, members, np.concatenate(toks))
+        logits[fuse] = torch.from_numpy(inst.logits())
+        inst.close()
+    assert (logits["1"] - logits["0"]).abs().max().item() <= 5e-2
+    oracle = FO.OracleModel(FO.with_layers(FO.QWEN25_7B, 2))
+    want = oracle.forward([(m.session_id, m.new_tokens, m.history) for m in members], toks)
+    d = (logits["1"] - want).abs()
+    assert d.max().item() <= 5e-2 and d.mean().item() <= 1e-2
