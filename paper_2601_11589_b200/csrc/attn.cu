@@ -1,26 +1,26 @@
 // Paged varlen prefill attention — see attn.cuh.
-// v1 math path: bf16 m16n8k16 warp MMAs with ldmatrix from XOR-swizzled
-// shared memory, cp.async double-buffered page loads, online softmax in fp32
-// (exp2 with the scale folded in), quad-shuffle row reductions.
+// Math path: bf16 m16n8k16 warp MMAs with ldmatrix from 128-byte-swizzled
+// shared memory (the TMA swizzle), online softmax in fp32 (exp2 with the scale
+// folded in), quad-shuffle row reductions. KV pages arrive by TMA
+// (cp.async.bulk.tensor.3d) into a 2-deep mbarrier ring; the Q tile (a gather
+// of (token, head) rows) is loaded once with cp.async.
 #include <cstdint>
+#include <stdexcept>
 
 #include "attn.cuh"
+#include "gemm_sm100.cuh"
 #include "launch.cuh"
+#include "ptx.cuh"
 
 namespace lp {
 
 namespace {
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
-               "l"(gmem));
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gmem));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N));
-}
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
                                         uint32_t& r3) {
@@ -46,68 +46,73 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// Row of D bf16 = D/8 16-byte chunks; chunk c of row r lives at c ^ (r & 7).
-template <int D>
+// 64 rows of D bf16, stored as D/64 "halves" of [64 rows][128 B] with the TMA
+// 128-byte swizzle: 16-byte chunk c of a row sits at (c ^ (row & 7)).
 __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
-  return base + row * (D * 2) + ((chunk ^ (row & 7)) << 4);
+  return base + (chunk >> 3) * (64 * 128) + row * 128 + (((chunk & 7) ^ (row & 7)) << 4);
 }
 
 template <int D>
 __global__ void __launch_bounds__(128)
-    attn_prefill_kernel(const AttnCtx c) {
+    attn_prefill_kernel(const __grid_constant__ CUtensorMap kvm, const AttnCtx c) {
   constexpr int kChunks = D / 8;           // 16-byte chunks per row
   constexpr int kTileBytes = 64 * D * 2;   // one page of one head
-  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int kHalves = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = smem + kTileBytes;          // [2][64][D]
-  uint8_t* sV = sK + 2 * kTileBytes;        // [2][64][D]
+  uint8_t* sK = smem + kTileBytes;          // [2][tile]
+  uint8_t* sV = sK + 2 * kTileBytes;        // [2][tile]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kTileBytes);
 
   pdl_trigger();
   const int wi = blockIdx.x;
   const bool live = wi < *c.n_work;  // written by the pre-graph H2D copy
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
   pdl_wait();
   if (!live) return;
   const int g = blockIdx.y;
   const int G = c.nq / c.nkv;
-  const int2 wk = c.work[wi];
+  const int4 wk = c.work[wi];
   const int r = wk.x, row0 = wk.y;
   const int L = c.q_len[r], H = c.hist[r], qs = c.q_start[r];
   const int rows_total = L * G;
-  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int* pages = c.page_list + c.page_off[r];
-  const size_t page_elems = static_cast<size_t>(2) * c.nkv * kAttnPage * D;
   const size_t ld_q = static_cast<size_t>(c.nq) * D;
 
+  const int row_hi = min(row0 + 63, rows_total - 1);
+  const int p_hi = H + row_hi / G;                  // max query position in CTA
+  const int p_lo = H + row0 / G;
+  const bool partial = wk.w >= 0;
+  const int t_begin = wk.z;
+  const int t_end = partial ? wk.w : (p_hi + 1 + 63) / 64;
+
+  auto issue_tile = [&](int kt, int buf) {
+    const int plane_k = c.kv_plane0 + pages[kt] * 2 * c.nkv + g;
+    mbar_arrive_expect_tx(&bars[buf], 2 * kTileBytes);
+#pragma unroll
+    for (int hf = 0; hf < kHalves; ++hf) {
+      tma_load_3d(sK + buf * kTileBytes + hf * 64 * 128, &kvm, &bars[buf], hf * 64, 0, plane_k);
+      tma_load_3d(sV + buf * kTileBytes + hf * 64 * 128, &kvm, &bars[buf], hf * 64, 0, plane_k + c.nkv);
+    }
+  };
+  if (tid == 0 && t_begin < t_end) issue_tile(t_begin, 0);
+
   // ---- Q tile -> smem (rows beyond the member replicate its last row) ----
-  const uint32_t sQa = static_cast<uint32_t>(__cvta_generic_to_shared(sQ));
+  const uint32_t sQa = smem_u32(sQ);
   for (int idx = tid; idx < 64 * kChunks; idx += 128) {
     const int rr = idx / kChunks, ch = idx % kChunks;
     const int row = min(row0 + rr, rows_total - 1);
     const int j = row / G, hq = g * G + row % G;
-    const __nv_bfloat16* src = c.q + (qs + j) * ld_q + hq * D + ch * 8;
-    cp_async16(sQ + (swz<D>(sQa, rr, ch) - sQa), src);
+    cp_async16(swz(sQa, rr, ch), c.q + (qs + j) * ld_q + hq * D + ch * 8);
   }
   cp_commit();
-
-  const int row_hi = min(row0 + 63, rows_total - 1);
-  const int p_hi = H + row_hi / G;                  // max query position in CTA
-  const int n_tiles = (p_hi + 1 + 63) / 64;
-  const int p_lo = H + row0 / G;
-
-  auto load_kv = [&](int kt, int buf) {
-    const size_t pbase = static_cast<size_t>(pages[kt]) * page_elems;
-    const __nv_bfloat16* kp = c.kv_layer + pbase + static_cast<size_t>(g) * kAttnPage * D;
-    const __nv_bfloat16* vp = c.kv_layer + pbase + static_cast<size_t>(c.nkv + g) * kAttnPage * D;
-    const uint32_t kb = static_cast<uint32_t>(__cvta_generic_to_shared(sK + buf * kTileBytes));
-    const uint32_t vb = static_cast<uint32_t>(__cvta_generic_to_shared(sV + buf * kTileBytes));
-    for (int idx = tid; idx < 64 * kChunks; idx += 128) {
-      const int rr = idx / kChunks, ch = idx % kChunks;
-      cp_async16(sK + buf * kTileBytes + (swz<D>(kb, rr, ch) - kb), kp + rr * D + ch * 8);
-      cp_async16(sV + buf * kTileBytes + (swz<D>(vb, rr, ch) - vb), vp + rr * D + ch * 8);
-    }
-    cp_commit();
-  };
-  load_kv(0, 0);
 
   // Per-thread rows: lane/4 and lane/4 + 8 of this warp's 16.
   const int my_row[2] = {row0 + warp * 16 + lane / 4, row0 + warp * 16 + lane / 4 + 8};
@@ -115,14 +120,14 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
   for (int i = 0; i < 2; ++i) my_pos[i] = H + min(my_row[i], rows_total - 1) / G;
 
-  cp_wait<1>();  // Q landed
+  cp_wait_all();
   __syncthreads();
   uint32_t qf[D / 16][4];
 #pragma unroll
   for (int ks = 0; ks < D / 16; ++ks) {
     const int rr = warp * 16 + (lane % 16);
     const int ch = ks * 2 + lane / 16;
-    ldsm_x4(swz<D>(sQa, rr, ch), qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3]);
+    ldsm_x4(swz(sQa, rr, ch), qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3]);
   }
 
   float o[D / 8][4];
@@ -130,17 +135,12 @@ __global__ void __launch_bounds__(128)
   for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
 
-  for (int kt = 0; kt < n_tiles; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < n_tiles) {
-      load_kv(kt + 1, buf ^ 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
-    const uint32_t kb = static_cast<uint32_t>(__cvta_generic_to_shared(sK + buf * kTileBytes));
-    const uint32_t vb = static_cast<uint32_t>(__cvta_generic_to_shared(sV + buf * kTileBytes));
+  for (int kt = t_begin; kt < t_end; ++kt) {
+    const int it = kt - t_begin, buf = it & 1;
+    if (tid == 0 && kt + 1 < t_end) issue_tile(kt + 1, buf ^ 1);  // buf^1 was released by the last barrier
+    mbar_wait(&bars[buf], (it >> 1) & 1);
+    const uint32_t kb = smem_u32(sK + buf * kTileBytes);
+    const uint32_t vb = smem_u32(sV + buf * kTileBytes);
 
     // S = Q K^T : 16 x 64 per warp.
     float s[8][4];
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(128)
         const int key = np * 16 + (mi / 2) * 8 + (lane % 8);
         const int ch = ks * 2 + (mi % 2);
         uint32_t b0, b1, b2, b3;
-        ldsm_x4(swz<D>(kb, key, ch), b0, b1, b2, b3);
+        ldsm_x4(swz(kb, key, ch), b0, b1, b2, b3);
         mma16816(s[2 * np], qf[ks], b0, b1);
         mma16816(s[2 * np + 1], qf[ks], b2, b3);
       }
@@ -171,7 +171,8 @@ __global__ void __launch_bounds__(128)
         }
       }
     }
-    // Online softmax (rows: e>>1 selects lane/4 or lane/4+8).
+    // Online softmax (rows: e>>1 selects lane/4 or lane/4+8). A split may
+    // hold no visible key for some rows: keep them at m = -inf, l = 0.
     float corr[2];
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
@@ -181,13 +182,14 @@ __global__ void __launch_bounds__(128)
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
       const float m_new = fmaxf(m_run[hr], mx * c.scale_log2);
-      corr[hr] = exp2f(m_run[hr] - m_new);
+      const float m_use = m_new == -INFINITY ? 0.f : m_new;
+      corr[hr] = exp2f(m_run[hr] - m_use);
       m_run[hr] = m_new;
       float sum = 0.f;
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
-        const float p0 = exp2f(s[nt][2 * hr] * c.scale_log2 - m_new);
-        const float p1 = exp2f(s[nt][2 * hr + 1] * c.scale_log2 - m_new);
+        const float p0 = exp2f(s[nt][2 * hr] * c.scale_log2 - m_use);
+        const float p1 = exp2f(s[nt][2 * hr + 1] * c.scale_log2 - m_use);
         s[nt][2 * hr] = p0;
         s[nt][2 * hr + 1] = p1;
         sum += p0 + p1;
@@ -217,47 +219,118 @@ __global__ void __launch_bounds__(128)
         const int key = ks * 16 + (mi % 2) * 8 + (lane % 8);
         const int ch = dp * 2 + (mi / 2);
         uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(swz<D>(vb, key, ch), b0, b1, b2, b3);
+        ldsm_x4_t(swz(vb, key, ch), b0, b1, b2, b3);
         mma16816(o[2 * dp], a, b0, b1);
         mma16816(o[2 * dp + 1], a, b2, b3);
       }
     }
-    __syncthreads();  // buffer `buf` is refilled next iteration
+    __syncthreads();  // every warp is done with `buf` before it is refilled
   }
 
-  // Normalise and store valid rows.
+  if (!partial) {
+    // Normalise and store valid rows.
 #pragma unroll
-  for (int hr = 0; hr < 2; ++hr) {
-    const int row = my_row[hr];
-    if (row >= rows_total || row > row0 + 63) continue;
-    const int j = row / G, hq = g * G + row % G;
-    const float inv = 1.f / l_run[hr];
-    __nv_bfloat16* dst = c.out + (qs + j) * ld_q + hq * D;
+    for (int hr = 0; hr < 2; ++hr) {
+      const int row = my_row[hr];
+      if (row >= rows_total) continue;
+      const int j = row / G, hq = g * G + row % G;
+      const float inv = 1.f / l_run[hr];
+      __nv_bfloat16* dst = c.out + (qs + j) * ld_q + hq * D;
 #pragma unroll
-    for (int nt = 0; nt < D / 8; ++nt) {
-      const int col = nt * 8 + (lane % 4) * 2;
-      *reinterpret_cast<uint32_t*>(dst + col) =
-          pack_bf16(o[nt][2 * hr] * inv, o[nt][2 * hr + 1] * inv);
+      for (int nt = 0; nt < D / 8; ++nt) {
+        const int col = nt * 8 + (lane % 4) * 2;
+        *reinterpret_cast<uint32_t*>(dst + col) = pack_bf16(o[nt][2 * hr] * inv, o[nt][2 * hr + 1] * inv);
+      }
+    }
+  } else {
+    // Unnormalised partial + (m, l) for the combine kernel.
+    const size_t slab = static_cast<size_t>(wi) * c.nkv + g;
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      const int rl = warp * 16 + lane / 4 + hr * 8;
+      float* dst = c.ws_o + (slab * 64 + rl) * D;
+#pragma unroll
+      for (int nt = 0; nt < D / 8; ++nt) {
+        const int col = nt * 8 + (lane % 4) * 2;
+        *reinterpret_cast<float2*>(dst + col) = make_float2(o[nt][2 * hr], o[nt][2 * hr + 1]);
+      }
+      if ((lane & 3) == 0) {
+        c.ws_ml[(slab * 64 + rl) * 2 + 0] = m_run[hr];
+        c.ws_ml[(slab * 64 + rl) * 2 + 1] = l_run[hr];
+      }
     }
   }
 }
 
+// Merge the key-range splits of one (row block, kv head): warp per row,
+// lanes over head_dim.
+template <int D>
+__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnCtx c) {
+  pdl_trigger();
+  const int ci = blockIdx.x;
+  const bool live = ci < *c.n_combine;
+  pdl_wait();
+  if (!live) return;
+  const int g = blockIdx.y;
+  const int G = c.nq / c.nkv;
+  const int4 e = c.combine[ci];
+  const int r = e.x, row0 = e.y, first = e.z, ns = e.w;
+  const int rows_total = c.q_len[r] * G, qs = c.q_start[r];
+  const size_t ld_q = static_cast<size_t>(c.nq) * D;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int rl = warp; rl < 64; rl += 4) {
+    const int row = row0 + rl;
+    if (row >= rows_total) break;
+    float m_star = -INFINITY;
+    for (int s = 0; s < ns; ++s)
+      m_star = fmaxf(m_star, c.ws_ml[((static_cast<size_t>(first + s) * c.nkv + g) * 64 + rl) * 2]);
+    float acc[D / 32];
+#pragma unroll
+    for (int k = 0; k < D / 32; ++k) acc[k] = 0.f;
+    float lsum = 0.f;
+    for (int s = 0; s < ns; ++s) {
+      const size_t slab = static_cast<size_t>(first + s) * c.nkv + g;
+      const float m = c.ws_ml[(slab * 64 + rl) * 2], l = c.ws_ml[(slab * 64 + rl) * 2 + 1];
+      const float w = m == -INFINITY ? 0.f : exp2f(m - m_star);
+      lsum += w * l;
+      const float* src = c.ws_o + (slab * 64 + rl) * D;
+#pragma unroll
+      for (int k = 0; k < D / 32; ++k) acc[k] += w * src[k * 32 + lane];
+    }
+    const int j = row / G, hq = g * G + row % G;
+    __nv_bfloat16* dst = c.out + (qs + j) * ld_q + hq * D;
+    const float inv = 1.f / lsum;
+#pragma unroll
+    for (int k = 0; k < D / 32; ++k) dst[k * 32 + lane] = __float2bfloat16_rn(acc[k] * inv);
+  }
+}
+
+template <int D>
+void launch(const AttnCtx& c, const CUtensorMap& kvm, int work_cap, int combine_cap, cudaStream_t st) {
+  constexpr int smem = 1024 + 5 * 64 * D * 2 + 64;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(attn_prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set = true;
+  }
+  launch_k(attn_prefill_kernel<D>, dim3(work_cap, c.nkv), dim3(128), smem, st, kvm, c);
+  launch_k(attn_combine_kernel<D>, dim3(combine_cap, c.nkv), dim3(128), 0, st, c);
+}
+
 }  // namespace
 
-void attention_prefill(const AttnCtx& c, int head_dim, int work_cap, cudaStream_t st) {
-  const dim3 grid(work_cap, c.nkv);
-  if (head_dim == 128) {
-    constexpr int smem = 5 * 64 * 128 * 2;
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(attn_prefill_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      set = true;
-    }
-    launch_k(attn_prefill_kernel<128>, grid, dim3(128), smem, st, c);
-  } else {
-    constexpr int smem = 5 * 64 * 64 * 2;
-    launch_k(attn_prefill_kernel<64>, grid, dim3(128), smem, st, c);
-  }
+CUtensorMap make_kv_tmap(const void* pool, int64_t planes, int head_dim) {
+  const uint64_t dims[3] = {static_cast<uint64_t>(head_dim), 64, static_cast<uint64_t>(planes)};
+  const uint64_t strides[2] = {static_cast<uint64_t>(head_dim) * 2, static_cast<uint64_t>(64) * head_dim * 2};
+  const uint32_t box[3] = {64, 64, 1};
+  return make_tmap_3d_bf16(pool, dims, strides, box);
+}
+
+void attention_prefill(const AttnCtx& c, const CUtensorMap& kv_map, int head_dim, int work_cap,
+                       int combine_cap, cudaStream_t st) {
+  if (head_dim == 128) launch<128>(c, kv_map, work_cap, combine_cap, st);
+  else if (head_dim == 64) launch<64>(c, kv_map, work_cap, combine_cap, st);
+  else throw std::runtime_error("attention: head_dim must be 64 or 128");
 }
 
 }  // namespace lp

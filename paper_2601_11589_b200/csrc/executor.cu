@@ -13,6 +13,7 @@ namespace lp {
 namespace {
 
 constexpr int kPage = kAttnPage;  // 64 tokens per KV page (== attention key tile)
+constexpr int kAttnSplitExtra = 2 * 148;  // extra attention work items for key-range splits
 
 // Tensor ids for the counter-based weight generator (oracle/forward_oracle.py
 // uses the same numbering).
@@ -157,7 +158,8 @@ void Instance::alloc_arena() {
   const int G = m_.n_q_heads / m_.n_kv_heads;
   t_max_ = static_cast<int>(d_.max_tokens);
   r_max_ = d_.max_members;
-  w_max_ = (t_max_ * G + kAttnRows - 1) / kAttnRows + r_max_;
+  c_max_ = (t_max_ * G + kAttnRows - 1) / kAttnRows + r_max_;
+  w_max_ = c_max_ + kAttnSplitExtra;
 
   x_resid_ = dmalloc<float>(size_t(t_max_) * h, allocs_);
   x_norm_ = dmalloc<bf16>(size_t(t_max_) * h, allocs_);
@@ -193,6 +195,10 @@ void Instance::alloc_arena() {
   layer_stride_ = page_elems_ * size_t(n_pages_);
   kv_pool_ = dmalloc<bf16>(layer_stride_ * m_.layers, allocs_);
   for (int32_t p = 0; p < n_pages_; ++p) free_pages_.insert(free_pages_.end(), p);
+  tm_kv_ = make_kv_tmap(kv_pool_, int64_t(m_.layers) * n_pages_ * 2 * m_.n_kv_heads, D);
+  // Key-range split partials: only the first kAttnSplitCap work items may be partial.
+  attn_ws_o_ = dmalloc<float>(size_t(kAttnSplitCap) * m_.n_kv_heads * kAttnRows * D, allocs_);
+  attn_ws_ml_ = dmalloc<float>(size_t(kAttnSplitCap) * m_.n_kv_heads * kAttnRows * 2, allocs_);
   max_pages_ = static_cast<int>(std::min<int64_t>(n_pages_, 4096));
 
   // Metadata block: device + pinned host mirror with identical layout.
@@ -205,7 +211,8 @@ void Instance::alloc_arena() {
   const size_t o_sc = carve(16 * 4), o_tok = carve(size_t(t_max_) * 4), o_pos = carve(size_t(t_max_) * 4),
                o_slot = carve(size_t(t_max_) * 4), o_qs = carve(r_max_ * 4), o_ql = carve(r_max_ * 4),
                o_h = carve(r_max_ * 4), o_li = carve(r_max_ * 4), o_po = carve(r_max_ * 4),
-               o_pt = carve(size_t(r_max_) * max_pages_ * 4), o_w = carve(size_t(w_max_) * 8);
+               o_pt = carve(size_t(r_max_) * max_pages_ * 4), o_w = carve(size_t(w_max_) * 16),
+               o_cb = carve(size_t(c_max_) * 16);
   meta_bytes_ = off;
   meta_dev_ = dmalloc<uint8_t>(meta_bytes_, allocs_);
   lp_check(cudaMallocHost(&meta_host_, meta_bytes_), "pinned meta");
@@ -222,12 +229,24 @@ void Instance::alloc_arena() {
     m.last_idx = reinterpret_cast<int*>(b + o_li);
     m.page_table = reinterpret_cast<int*>(b + o_pt);
     m.page_off = reinterpret_cast<int*>(b + o_po);
-    m.work = reinterpret_cast<int2*>(b + o_w);
+    m.work = reinterpret_cast<int4*>(b + o_w);
+    m.combine = reinterpret_cast<int4*>(b + o_cb);
   };
   bind(meta_dev_, md_);
   bind(meta_host_, mh_);
   lp_check(cudaMemsetAsync(meta_dev_, 0, meta_bytes_, stream_), "meta zero");
   lp_check(cudaStreamSynchronize(stream_), "arena sync");
+}
+
+// Attention grid capacities for a forward launched at (t_cap, r_cap): one
+// item per 64-row block of (token, q-head) rows of each member, plus room for
+// key-range splits of short batches over long histories.
+int Instance::combine_cap_for(int t_cap, int r_cap) const {
+  const int G = m_.n_q_heads / m_.n_kv_heads;
+  return std::min(c_max_, (t_cap * G + kAttnRows - 1) / kAttnRows + r_cap);
+}
+int Instance::work_cap_for(int t_cap, int r_cap) const {
+  return std::min(w_max_, combine_cap_for(t_cap, r_cap) + kAttnSplitExtra);
 }
 
 SplitPlan Instance::plan_for(int t_cap, int r_cap) const {
@@ -265,7 +284,9 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st) {
   const int* n_mem = md_.scalars + 1;
   const RowCtx rc{n_tok, t_cap, h, m_.rms_eps};
   const int G = nq / nkv;
-  const int work_cap = std::min(w_max_, (t_cap * G + kAttnRows - 1) / kAttnRows + r_cap);
+  const int work_cap = work_cap_for(t_cap, r_cap);
+  const int combine_cap = combine_cap_for(t_cap, r_cap);
+  (void)G;
 
   embed_rmsnorm(rc, md_.tokens, embed_, layers_[0].g_attn, x_resid_, x_norm_, st);
   for (int l = 0; l < m_.layers; ++l) {
@@ -287,10 +308,11 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st) {
                 md_.positions, md_.slots, inv_freq_, q_, kv_layer};
       qkv_post(qc, st);
     }
-    AttnCtx ac{md_.scalars + 2, md_.work, md_.q_start, md_.q_len, md_.hist, md_.page_table,
-               md_.page_off, q_, kv_layer, attn_, nq, nkv,
+    AttnCtx ac{md_.scalars + 2, md_.work, md_.scalars + 3, md_.combine, md_.q_start, md_.q_len, md_.hist,
+               md_.page_table, md_.page_off, q_, static_cast<int>(int64_t(l) * n_pages_ * 2 * nkv), attn_,
+               attn_ws_o_, attn_ws_ml_, nq, nkv,
                static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)))};
-    attention_prefill(ac, D, work_cap, st);
+    attention_prefill(ac, tm_kv_, D, work_cap, combine_cap, st);
     // O projection + residual + RMSNorm.
     g = GemmArgs{};
     g.M = h; g.N = t_cap; g.K = nq * D; g.n_dev = n_tok;
@@ -356,7 +378,7 @@ void Instance::capture_graphs(const std::vector<int64_t>& lens, const std::vecto
   if (!d_.use_graphs) return;
   lp_check(cudaSetDevice(d_.device), "set device");
   // Warm the launch paths (function attributes, tensor-map cache) eagerly.
-  mh_.scalars[0] = mh_.scalars[1] = mh_.scalars[2] = 0;
+  mh_.scalars[0] = mh_.scalars[1] = mh_.scalars[2] = mh_.scalars[3] = 0;
   lp_check(cudaMemcpyAsync(md_.scalars, mh_.scalars, 16, cudaMemcpyHostToDevice, stream_), "meta");
   for (int64_t L : lens) {
     for (int32_t dep : depths) {
@@ -411,7 +433,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
 
   // Host metadata.
   const int G = m_.n_q_heads / m_.n_kv_heads;
-  int t = 0, nw = 0, np = 0;
+  int t = 0, np = 0;
   for (int i = 0; i < n; ++i) {
     const Session& s = sessions_[mem[i].session_id];
     const int L = static_cast<int>(mem[i].new_tokens), H = static_cast<int>(mem[i].history);
@@ -429,11 +451,55 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
       mh_.positions[t] = pos;
       mh_.slots[t] = s.pages[pos / kPage] * kPage + pos % kPage;
     }
-    for (int r0 = 0; r0 < L * G; r0 += kAttnRows) mh_.work[nw++] = make_int2(i, r0);
   }
+
+  // Which launch runs this batch (fixes the attention grid capacity).
+  auto it = (shape.kind == LP_KIND_GRAPH && d_.use_graphs) ? graphs_.find(graph_key(shape.l_pad, shape.depth))
+                                                           : graphs_.end();
+  const int t_cap = it != graphs_.end() ? static_cast<int>(shape.l_pad * shape.depth)
+                                        : std::min(std::max(16, (t + 15) / 16 * 16), t_max_);
+  const int r_cap = it != graphs_.end() ? shape.depth : n;
+  const int work_cap = work_cap_for(t_cap, r_cap);
+
+  // Attention work list: one item per 64-row block of (token, q-head) rows;
+  // when the blocks cannot fill the GPU, long key ranges are split
+  // (>= kMinSplitTiles pages each) and merged by the combine kernel. Split
+  // (partial) items come first so their indices address the partial
+  // workspace; the rest follow heaviest first.
+  struct Blk {
+    int r, row0, need;
+  };
+  std::vector<Blk> blks;
+  for (int i = 0; i < n; ++i) {
+    const int L = mh_.q_len[i], H = mh_.hist[i];
+    for (int r0 = 0; r0 < L * G; r0 += kAttnRows) {
+      const int p_hi = H + std::min(r0 + kAttnRows - 1, L * G - 1) / G;
+      blks.push_back({i, r0, (p_hi + 1 + kPage - 1) / kPage});
+    }
+  }
+  std::stable_sort(blks.begin(), blks.end(), [](const Blk& a, const Blk& b) { return a.need > b.need; });
+  constexpr int kMinSplitTiles = 8;
+  const int base = static_cast<int>(blks.size());
+  const int ctas = base * m_.n_kv_heads, target = 2 * num_sms();
+  const int f = ctas < target ? (target + ctas - 1) / ctas : 1;
+  int nw = 0, nc = 0, n_items = base;
+  std::vector<Blk> full;
+  for (const Blk& b : blks) {
+    const int s = std::min(f, b.need / kMinSplitTiles);
+    if (s >= 2 && nw + s <= kAttnSplitCap && n_items + s - 1 <= work_cap) {
+      mh_.combine[nc++] = make_int4(b.r, b.row0, nw, s);
+      for (int k = 0; k < s; ++k)
+        mh_.work[nw++] = make_int4(b.r, b.row0, k * b.need / s, (k + 1) * b.need / s);
+      n_items += s - 1;
+    } else {
+      full.push_back(b);
+    }
+  }
+  for (const Blk& b : full) mh_.work[nw++] = make_int4(b.r, b.row0, 0, -1);
   mh_.scalars[0] = t;
   mh_.scalars[1] = n;
   mh_.scalars[2] = nw;
+  mh_.scalars[3] = nc;
 
   last_h2d_bytes_ = 0;
   auto h2d = [&](void* dst, const void* src, size_t bytes) {
@@ -450,18 +516,16 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   h2d(md_.last_idx, mh_.last_idx, size_t(n) * 4);
   h2d(md_.page_off, mh_.page_off, size_t(n) * 4);
   h2d(md_.page_table, mh_.page_table, size_t(np) * 4);
-  h2d(md_.work, mh_.work, size_t(nw) * 8);
+  h2d(md_.work, mh_.work, size_t(nw) * 16);
+  h2d(md_.combine, mh_.combine, size_t(nc) * 16);
 
   lp_check(cudaEventRecord(ev_h2d_, stream_), "event");
   lp_check(cudaEventRecord(ev_start_, stream_), "event");
-  auto it = (shape.kind == LP_KIND_GRAPH && d_.use_graphs) ? graphs_.find(graph_key(shape.l_pad, shape.depth))
-                                                           : graphs_.end();
   if (it != graphs_.end()) {
     lp_check(cudaGraphLaunch(it->second, stream_), "graph launch");
   } else {
     // Standard / packed / uncaptured: eager launch sized to the live batch.
-    const int t_cap = std::max(16, (t + 15) / 16 * 16);
-    enqueue_forward(std::min(t_cap, t_max_), n, stream_);
+    enqueue_forward(t_cap, r_cap, stream_);
   }
   lp_check(cudaGetLastError(), "forward launch");
   lp_check(cudaEventRecord(ev_end_, stream_), "event");

@@ -51,7 +51,8 @@ struct Meta {
   int* last_idx;    // [R]
   int* page_table;  // flattened page ids of all members (ragged)
   int* page_off;    // [R] offset of member r in page_table
-  int2* work;       // [W]
+  int4* work;       // [W] attention work items (see attn.cuh)
+  int4* combine;    // [C] split row blocks to merge
 };
 
 // Launch plan of one projection at a given token capacity.
@@ -119,7 +120,12 @@ class Instance {
   int max_pages_ = 0;  // page-table row stride
 
   // arena
-  int t_max_ = 0, r_max_ = 0, w_max_ = 0;
+  int t_max_ = 0, r_max_ = 0, w_max_ = 0, c_max_ = 0;
+  float* attn_ws_o_ = nullptr;
+  float* attn_ws_ml_ = nullptr;
+  CUtensorMap tm_kv_;
+  int work_cap_for(int t_cap, int r_cap) const;
+  int combine_cap_for(int t_cap, int r_cap) const;
   float* x_resid_ = nullptr;
   bf16 *x_norm_ = nullptr, *q_ = nullptr, *attn_ = nullptr, *act_ = nullptr, *x_last_ = nullptr;
   float* ws_ = nullptr;

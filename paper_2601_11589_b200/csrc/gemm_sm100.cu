@@ -455,6 +455,22 @@ CUtensorMap make_tmap_bf16(const void* ptr, uint64_t rows, uint64_t cols, uint32
 
 int gemm_b_box_rows(int bn, int pair) { return bn / pair; }
 
+CUtensorMap make_tmap_3d_bf16(const void* ptr, const uint64_t dims[3], const uint64_t strides_bytes[2],
+                              const uint32_t box[3]) {
+  CUtensorMap m;
+  const cuuint64_t d[3] = {dims[0], dims[1], dims[2]};
+  const cuuint64_t s[2] = {strides_bytes[0], strides_bytes[1]};
+  const cuuint32_t b[3] = {box[0], box[1], box[2]};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), d, s, b,
+                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    throw std::runtime_error("cuTensorMapEncodeTiled (3d) failed: " + std::to_string(static_cast<int>(r)));
+  }
+  return m;
+}
+
 void gemm_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, int bn,
                  cudaStream_t stream, int max_ctas, int pair) {
   if (a.M % (kBM * pair) != 0 || a.K % kBK != 0 || a.N < 1 || a.splits < 1) {

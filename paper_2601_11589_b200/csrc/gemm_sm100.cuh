@@ -57,6 +57,9 @@ struct GemmArgs {
 // Build a 2D bf16 tensor map over a row-major [rows, cols] matrix, box
 // [box_rows, 64 cols], 128-byte swizzle.
 CUtensorMap make_tmap_bf16(const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+// 3-D bf16 tensor map, 128-byte swizzle (dims innermost first).
+CUtensorMap make_tmap_3d_bf16(const void* ptr, const uint64_t dims[3], const uint64_t strides_bytes[2],
+                              const uint32_t box[3]);
 
 // Launch. `bn` is the token-tile width (16, 32, 64, 128 or 256). pair = 2
 // selects the CTA-pair (cta_group::2, M = 256 per pair) variant; M must then
