@@ -262,10 +262,12 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// Merge the key-range splits of one (row block, kv head): warp per row,
-// lanes over head_dim.
+// Merge the key-range splits of one (row block, kv head). Grid (groups, nkv,
+// block_rows / 32), 8 warps x 4 rows; per row, lane s fetches split s's
+// (m, l) (<= 32 splits), weights come from warp reductions, and the partial
+// O rows are read with every split's loads in flight.
 template <int D>
-__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnCtx c) {
+__global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCtx c) {
   pdl_trigger();
   const int ci = blockIdx.x;
   const bool live = ci < *c.n_combine;
@@ -278,22 +280,30 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnCtx c) {
   const int rows_total = c.q_len[r] * G, qs = c.q_start[r];
   const size_t ld_q = static_cast<size_t>(c.nq) * D;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  for (int rl = warp; rl < 64; rl += 4) {
+  const int br = c.block_rows;
+  for (int i = 0; i < 4; ++i) {
+    const int rl = blockIdx.z * 32 + warp * 4 + i;
     const int row = row0 + rl;
-    if (row >= rows_total) break;
-    float m_star = -INFINITY;
-    for (int s = 0; s < ns; ++s)
-      m_star = fmaxf(m_star, c.ws_ml[((static_cast<size_t>(first + s) * c.nkv + g) * 64 + rl) * 2]);
+    if (rl >= br || row >= rows_total) break;
+    float m = -INFINITY, l = 0.f;
+    if (lane < ns) {
+      const size_t slab = static_cast<size_t>(first + lane) * c.nkv + g;
+      m = c.ws_ml[(slab * br + rl) * 2];
+      l = c.ws_ml[(slab * br + rl) * 2 + 1];
+    }
+    float m_star = m;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m_star = fmaxf(m_star, __shfl_xor_sync(0xffffffffu, m_star, o));
+    const float w_mine = (lane < ns && m != -INFINITY) ? exp2f(m - m_star) : 0.f;
+    float lsum = w_mine * l;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
     float acc[D / 32];
 #pragma unroll
     for (int k = 0; k < D / 32; ++k) acc[k] = 0.f;
-    float lsum = 0.f;
     for (int s = 0; s < ns; ++s) {
-      const size_t slab = static_cast<size_t>(first + s) * c.nkv + g;
-      const float m = c.ws_ml[(slab * 64 + rl) * 2], l = c.ws_ml[(slab * 64 + rl) * 2 + 1];
-      const float w = m == -INFINITY ? 0.f : exp2f(m - m_star);
-      lsum += w * l;
-      const float* src = c.ws_o + (slab * 64 + rl) * D;
+      const float w = __shfl_sync(0xffffffffu, w_mine, s);
+      const float* src = c.ws_o + ((static_cast<size_t>(first + s) * c.nkv + g) * br + rl) * D;
 #pragma unroll
       for (int k = 0; k < D / 32; ++k) acc[k] += w * src[k * 32 + lane];
     }
@@ -314,7 +324,7 @@ void launch(const AttnCtx& c, const CUtensorMap& kvm, int work_cap, int combine_
     set = true;
   }
   launch_k(attn_prefill_kernel<D>, dim3(work_cap, c.nkv), dim3(128), smem, st, kvm, c);
-  launch_k(attn_combine_kernel<D>, dim3(combine_cap, c.nkv), dim3(128), 0, st, c);
+  launch_k(attn_combine_kernel<D>, dim3(combine_cap, c.nkv, c.block_rows / 32), dim3(256), 0, st, c);
 }
 
 }  // namespace
@@ -328,9 +338,16 @@ CUtensorMap make_kv_tmap(const void* pool, int64_t planes, int head_dim) {
 
 void attention_prefill(const AttnCtx& c, const CUtensorMap& kv_map, int head_dim, int work_cap,
                        int combine_cap, cudaStream_t st) {
-  if (head_dim == 128) launch<128>(c, kv_map, work_cap, combine_cap, st);
-  else if (head_dim == 64) launch<64>(c, kv_map, work_cap, combine_cap, st);
-  else throw std::runtime_error("attention: head_dim must be 64 or 128");
+  if (head_dim == 128 && c.block_rows == kAttnTcRows) {
+    attention_prefill_tc(c, kv_map, work_cap, st);
+    launch_k(attn_combine_kernel<128>, dim3(combine_cap, c.nkv, c.block_rows / 32), dim3(256), 0, st, c);
+  } else if (head_dim == 128) {
+    launch<128>(c, kv_map, work_cap, combine_cap, st);
+  } else if (head_dim == 64) {
+    launch<64>(c, kv_map, work_cap, combine_cap, st);
+  } else {
+    throw std::runtime_error("attention: head_dim must be 64 or 128");
+  }
 }
 
 }  // namespace lp

@@ -42,11 +42,13 @@ struct AttnCtx {
   float* ws_ml;                  // [W][nkv][64][2] running max (log2 units) and sum
   int nq, nkv;
   float scale_log2;  // log2(e) / sqrt(d)
+  int block_rows;    // rows per work item: 64 (warp-MMA kernel) or 128 (tcgen05 kernel)
 };
 
 constexpr int kAttnRows = 64;    // rows per CTA
 constexpr int kAttnPage = 64;    // required page size (== key tile)
 constexpr int kAttnSplitCap = 1024;  // max split (partial) work items per forward
+constexpr int kAttnTcRows = 128;     // rows per CTA of the tcgen05 kernel (head_dim 128)
 
 // TMA map over the whole paged pool viewed as [planes][64 slots][d] bf16,
 // plane = (layer * n_pages + page) * 2 * nkv + (is_v * nkv + kv_head).
@@ -55,5 +57,7 @@ CUtensorMap make_kv_tmap(const void* pool, int64_t planes, int head_dim);
 // grid_x = work capacity, grid_y = nkv. head_dim in {64, 128}.
 void attention_prefill(const AttnCtx& c, const CUtensorMap& kv_map, int head_dim, int work_cap,
                        int combine_cap, cudaStream_t st);
+// tcgen05/TMEM kernel (head_dim 128, block_rows 128); see attn_tc.cu.
+void attention_prefill_tc(const AttnCtx& c, const CUtensorMap& kv_map, int work_cap, cudaStream_t st);
 
 }  // namespace lp

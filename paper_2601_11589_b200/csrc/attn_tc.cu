@@ -1,0 +1,327 @@
+// tcgen05/TMEM prefill attention (head_dim 128) — the dense path for long
+// prompts and deep batches (north_star subsystem 2: "tcgen05/TMEM bf16 GEMMs
+// ... and for long-prompt attention").
+//
+// One CTA = 128 packed (token, q-head) rows of one KV group x a key range.
+// Roles (192 threads):
+//   warp 0   TMA producer: K and V pages (2 pages = 128 keys per step) into a
+//            2-stage ring, laid out [d-half][128 keys][128 B] (128B swizzle);
+//   warp 1   MMA issuer (one thread):  S = Q K^T into TMEM (double-buffered,
+//            so S(j+1) overlaps the softmax of j), then O += P V with V as an
+//            MN-major operand (no transpose pass) and O resident in TMEM;
+//   warps 2-5 softmax: thread = query row = TMEM lane. tcgen05.ld of its S
+//            row, causal mask, online softmax in the log2 domain, P -> smem
+//            (bf16, 128B swizzle), O rescaled in TMEM only when the row max
+//            grew; epilogue O / l -> bf16 (or fp32 partial for key splits).
+// Numerics match the mma.sync path (and the oracle's storage points): fp32
+// scores, bf16 P, fp32 O accumulation; key tiles of 128 instead of 64 change
+// only the online-softmax rescale points.
+#include <cstdint>
+#include <stdexcept>
+
+#include "attn.cuh"
+#include "launch.cuh"
+#include "ptx.cuh"
+
+namespace lp {
+
+namespace {
+
+constexpr int kD = 128;
+constexpr int kRows = 128;
+constexpr int kKeys = 128;                 // keys per step (2 pages)
+constexpr int kHalfBytes = kRows * 128;    // [128 rows][64 elems] bf16 = 16 KiB
+constexpr int kQBytes = 2 * kHalfBytes;    // Q / P / K / V tile: 32 KiB each
+constexpr int kStages = 2;
+constexpr int kThreads = 192;
+
+struct TcSmem {
+  static constexpr int kQ = 0;
+  static constexpr int kP = kQ + kQBytes;
+  static constexpr int kK = kP + kQBytes;                 // [stage][32 KiB]
+  static constexpr int kV = kK + kStages * kQBytes;       // [stage][32 KiB]
+  static constexpr int kBars = kV + kStages * kQBytes;
+  static constexpr int kTotal = kBars + 256;
+};
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gmem));
+}
+
+// K-major 128B-swizzled [2 halves][128 rows][128 B] tile: 16-byte chunk c
+// (0..15) of row r.
+__device__ __forceinline__ uint32_t tile_addr(uint32_t base, int r, int c) {
+  return base + (c >> 3) * kHalfBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap kvm, const AttnCtx c) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TcSmem::kBars);
+  uint64_t* kv_full = bars;        // [2]
+  uint64_t* kv_empty = bars + 2;   // [2]
+  uint64_t* s_full = bars + 4;     // [2]
+  uint64_t* s_empty = bars + 6;    // [2]
+  uint64_t* p_ready = bars + 8;
+  uint64_t* o_done = bars + 9;
+  uint64_t* q_ready = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  pdl_trigger();
+  const int wi = blockIdx.x;
+  const bool live = wi < *c.n_work;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+    }
+    mbar_init(p_ready, 4);
+    mbar_init(o_done, 1);
+    mbar_init(q_ready, 4);
+    fence_mbar_init();
+  }
+  if (warp == 1 && live) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (!live) {
+    pdl_wait();
+    return;
+  }
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+
+  const int g = blockIdx.y;
+  const int G = c.nq / c.nkv;
+  const int4 wk = c.work[wi];
+  const int r = wk.x, row0 = wk.y;
+  const int L = c.q_len[r], H = c.hist[r], qs = c.q_start[r];
+  const int rows_total = L * G;
+  const int* pages = c.page_list + c.page_off[r];
+  const size_t ld_q = static_cast<size_t>(c.nq) * kD;
+  const int row_hi = min(row0 + kRows - 1, rows_total - 1);
+  const int p_hi = H + row_hi / G;
+  const bool partial = wk.w >= 0;
+  const int t_begin = wk.z;                               // first page
+  const int t_end = partial ? wk.w : (p_hi + 1 + 63) / 64;  // one past the last page
+  const int n_steps = (t_end - t_begin + 1) / 2;
+
+  const uint32_t sQ = smem_u32(smem + TcSmem::kQ), sP = smem_u32(smem + TcSmem::kP);
+  const uint32_t sK = smem_u32(smem + TcSmem::kK), sV = smem_u32(smem + TcSmem::kV);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      for (int s = 0; s < n_steps; ++s) {
+        const int st = s & 1;
+        mbar_wait(&kv_empty[st], ((s >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * kQBytes);
+        const int t0 = t_begin + 2 * s;
+        // A missing second page re-loads the first (finite values, masked).
+        const int pg[2] = {pages[t0], t0 + 1 < t_end ? pages[t0 + 1] : pages[t0]};
+#pragma unroll
+        for (int pi = 0; pi < 2; ++pi) {
+          const int plane_k = c.kv_plane0 + pg[pi] * 2 * c.nkv + g;
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            uint8_t* dk = smem + TcSmem::kK + st * kQBytes + hf * kHalfBytes + pi * 64 * 128;
+            uint8_t* dv = smem + TcSmem::kV + st * kQBytes + hf * kHalfBytes + pi * 64 * 128;
+            tma_load_3d(dk, &kvm, &kv_full[st], hf * 64, 0, plane_k);
+            tma_load_3d(dv, &kvm, &kv_full[st], hf * 64, 0, plane_k + c.nkv);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc_s = idesc_bf16(kRows, kKeys);
+    constexpr uint32_t idesc_o = idesc_bf16(kRows, kD) | (1u << 16);  // B (V) is MN-major
+    const uint32_t t_o = tmem + 2 * kKeys;
+    mbar_wait(q_ready, 0);
+    tc_fence_after();
+    auto issue_s = [&](int s) {
+      const int st = s & 1;
+      mbar_wait(&kv_full[st], (s >> 1) & 1);
+      if (s >= 2) mbar_wait(&s_empty[st], ((s >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) {
+          const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
+          tc_mma_bf16(tmem + st * kKeys, sdesc_sw128(sQ + off), sdesc_sw128(sK + st * kQBytes + off), idesc_s,
+                      k > 0 ? 1u : 0u);
+        }
+        tc_commit(&s_full[st]);
+      }
+      __syncwarp();
+    };
+    if (n_steps > 0) issue_s(0);
+    for (int s = 0; s < n_steps; ++s) {
+      const int st = s & 1;
+      if (s + 1 < n_steps) issue_s(s + 1);
+      mbar_wait(p_ready, s & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < kKeys / 16; ++k) {
+          const uint64_t a = sdesc_sw128(sP + (k >> 2) * kHalfBytes + (k & 3) * 32);
+          const uint64_t b = sdesc_sw128_mn(sV + st * kQBytes + k * 16 * 128, kHalfBytes, 1024);
+          tc_mma_bf16(t_o, a, b, idesc_o, (s > 0 || k > 0) ? 1u : 0u);
+        }
+        tc_commit(o_done);
+        tc_commit(&kv_empty[st]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue
+    const int q4 = warp & 3;
+    const int rt = q4 * 32 + lane;             // tile row == TMEM lane
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const int row = min(row0 + rt, rows_total - 1);
+    const int j = row / G, hq = g * G + row % G;
+    const int pos = H + j;
+    // Q row -> smem (swizzled), once.
+    const __nv_bfloat16* qrow = c.q + (qs + j) * ld_q + hq * kD;
+#pragma unroll
+    for (int ch = 0; ch < 16; ++ch) cp_async16(tile_addr(sQ, rt, ch), qrow + ch * 8);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(q_ready);
+
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int s = 0; s < n_steps; ++s) {
+      const int st = s & 1;
+      mbar_wait(&s_full[st], (s >> 1) & 1);
+      tc_fence_after();
+      float sc[kKeys];
+#pragma unroll
+      for (int cc = 0; cc < kKeys / 16; ++cc) tmem_ld16(tmem + lane_off + st * kKeys + cc * 16, sc + cc * 16);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[st]);  // S buffer may be overwritten
+
+      const int kbase = (t_begin + 2 * s) * 64;
+      const int kvalid = min(kKeys, (t_end - t_begin - 2 * s) * 64);  // keys of real pages in this step
+      float mx = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < kKeys; ++k) {
+        if (k >= kvalid || kbase + k > pos) sc[k] = -INFINITY;
+        mx = fmaxf(mx, sc[k]);
+      }
+      const float m_new = fmaxf(m_run, mx * c.scale_log2);
+      const float m_use = m_new == -INFINITY ? 0.f : m_new;
+      const float corr = exp2f(m_run - m_use);
+      m_run = m_new;
+      float sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < kKeys; ++k) {
+        sc[k] = exp2f(sc[k] * c.scale_log2 - m_use);
+        sum += sc[k];
+      }
+      l_run = l_run * corr + sum;
+
+      // PV(s-1) must be complete before P is overwritten and O rescaled.
+      if (s > 0) {
+        mbar_wait(o_done, (s - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, corr != 1.f)) {
+          const uint32_t t_o = tmem + lane_off + 2 * kKeys;
+#pragma unroll 1
+          for (int cc = 0; cc < kD / 16; ++cc) {
+            float o[16];
+            tmem_ld16(t_o + cc * 16, o);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] *= corr;
+            tmem_st16(t_o + cc * 16, o);
+          }
+          tc_wait_st();
+        }
+      }
+      // P row (bf16) -> smem in the swizzled K-major layout of the A operand.
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {
+        uint4 w;
+        w.x = pack_bf16x2(sc[ch * 8 + 0], sc[ch * 8 + 1]);
+        w.y = pack_bf16x2(sc[ch * 8 + 2], sc[ch * 8 + 3]);
+        w.z = pack_bf16x2(sc[ch * 8 + 4], sc[ch * 8 + 5]);
+        w.w = pack_bf16x2(sc[ch * 8 + 6], sc[ch * 8 + 7]);
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(tile_addr(sP, rt, ch)), "r"(w.x), "r"(w.y),
+                     "r"(w.z), "r"(w.w)
+                     : "memory");
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_ready);
+    }
+
+    // Epilogue: O row / l.
+    if (n_steps > 0) {
+      mbar_wait(o_done, (n_steps - 1) & 1);
+      tc_fence_after();
+    }
+    const uint32_t t_o = tmem + lane_off + 2 * kKeys;
+    if (!partial) {
+      const float inv = 1.f / l_run;
+      __nv_bfloat16* dst = c.out + (qs + j) * ld_q + hq * kD;
+#pragma unroll 1
+      for (int cc = 0; cc < kD / 16; ++cc) {
+        float o[16];
+        tmem_ld16(t_o + cc * 16, o);
+        if (row0 + rt < rows_total) {
+          uint4 w[2];
+          uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) wp[i] = pack_bf16x2(o[2 * i] * inv, o[2 * i + 1] * inv);
+          reinterpret_cast<uint4*>(dst + cc * 16)[0] = w[0];
+          reinterpret_cast<uint4*>(dst + cc * 16)[1] = w[1];
+        }
+      }
+    } else {
+      const size_t slab = static_cast<size_t>(wi) * c.nkv + g;
+      float* dst = c.ws_o + (slab * kRows + rt) * kD;
+#pragma unroll 1
+      for (int cc = 0; cc < kD / 16; ++cc) {
+        float o[16];
+        tmem_ld16(t_o + cc * 16, o);
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(dst + cc * 16 + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+      }
+      c.ws_ml[(slab * kRows + rt) * 2 + 0] = m_run;
+      c.ws_ml[(slab * kRows + rt) * 2 + 1] = l_run;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+void attention_prefill_tc(const AttnCtx& c, const CUtensorMap& kv_map, int work_cap, cudaStream_t st) {
+  constexpr int smem = 1024 + TcSmem::kTotal;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set = true;
+  }
+  launch_k(attn_tc_kernel, dim3(work_cap, c.nkv), dim3(kThreads), smem, st, kv_map, c);
+}
+
+}  // namespace lp

@@ -80,6 +80,7 @@ Instance::Instance(const lp_model_desc& m, const lp_instance_desc& d) : m_(m), d
   if (d_.max_tokens <= 0) d_.max_tokens = 16384;
   if (d_.max_members <= 0) d_.max_members = 64;
   if (const char* e = std::getenv("LP_FUSE_EPI"); e && e[0] == '0') fuse_epilogues_ = false;
+  if (const char* e = std::getenv("LP_ATTN_TC"); e && e[0] == '0') attn_tc_ = false;
   lp_check(cudaSetDevice(d.device), "cudaSetDevice");
   lp_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   lp_check(cudaEventCreate(&ev_start_), "event");
@@ -197,8 +198,13 @@ void Instance::alloc_arena() {
   for (int32_t p = 0; p < n_pages_; ++p) free_pages_.insert(free_pages_.end(), p);
   tm_kv_ = make_kv_tmap(kv_pool_, int64_t(m_.layers) * n_pages_ * 2 * m_.n_kv_heads, D);
   // Key-range split partials: only the first kAttnSplitCap work items may be partial.
-  attn_ws_o_ = dmalloc<float>(size_t(kAttnSplitCap) * m_.n_kv_heads * kAttnRows * D, allocs_);
-  attn_ws_ml_ = dmalloc<float>(size_t(kAttnSplitCap) * m_.n_kv_heads * kAttnRows * 2, allocs_);
+  // Eager launches (long chunks, off-grid / packed batches: long key ranges,
+  // many rows) use the tcgen05 kernel; graph replays (<= 256 new tokens per
+  // member) keep the lighter warp-MMA kernel, whose per-CTA fixed cost is
+  // lower for one or two key tiles. The kernel is fixed at capture time.
+  attn_rows_ = (D == 128 && attn_tc_) ? kAttnTcRows : kAttnRows;
+  attn_ws_o_ = dmalloc<float>(size_t(kAttnSplitCap) * m_.n_kv_heads * attn_rows_ * D, allocs_);
+  attn_ws_ml_ = dmalloc<float>(size_t(kAttnSplitCap) * m_.n_kv_heads * attn_rows_ * 2, allocs_);
   max_pages_ = static_cast<int>(std::min<int64_t>(n_pages_, 4096));
 
   // Metadata block: device + pinned host mirror with identical layout.
@@ -275,7 +281,8 @@ void Instance::gemm(const CUtensorMap& tm_w, const GemmPlan& p, GemmArgs g, cons
   gemm_launch(tm_w, act_map(x, x_rows, g.K, gemm_b_box_rows(p.bn, p.pair)), g, p.bn, st, 0, p.pair);
 }
 
-void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st) {
+void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph) {
+  const int attn_rows = graph ? kAttnRows : attn_rows_;
   const int h = m_.hidden, I = m_.intermediate, D = m_.head_dim;
   const int nq = m_.n_q_heads, nkv = m_.n_kv_heads;
   const int qkv_out = (nq + 2 * nkv) * D;
@@ -311,7 +318,7 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st) {
     AttnCtx ac{md_.scalars + 2, md_.work, md_.scalars + 3, md_.combine, md_.q_start, md_.q_len, md_.hist,
                md_.page_table, md_.page_off, q_, static_cast<int>(int64_t(l) * n_pages_ * 2 * nkv), attn_,
                attn_ws_o_, attn_ws_ml_, nq, nkv,
-               static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)))};
+               static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D))), attn_rows};
     attention_prefill(ac, tm_kv_, D, work_cap, combine_cap, st);
     // O projection + residual + RMSNorm.
     g = GemmArgs{};
@@ -386,10 +393,10 @@ void Instance::capture_graphs(const std::vector<int64_t>& lens, const std::vecto
       if (t_cap > t_max_ || dep > r_max_) continue;
       const int64_t key = graph_key(L, dep);
       if (graphs_.count(key)) continue;
-      enqueue_forward(static_cast<int>(t_cap), dep, stream_);  // eager warm-up (no live work)
+      enqueue_forward(static_cast<int>(t_cap), dep, stream_, true);  // warm-up (no live work)
       cudaGraph_t graph;
       lp_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
-      enqueue_forward(static_cast<int>(t_cap), dep, stream_);
+      enqueue_forward(static_cast<int>(t_cap), dep, stream_, true);
       lp_check(cudaStreamEndCapture(stream_, &graph), "end capture");
       cudaGraphExec_t exec;
       lp_check(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
@@ -460,6 +467,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
                                         : std::min(std::max(16, (t + 15) / 16 * 16), t_max_);
   const int r_cap = it != graphs_.end() ? shape.depth : n;
   const int work_cap = work_cap_for(t_cap, r_cap);
+  const int attn_rows = it != graphs_.end() ? kAttnRows : attn_rows_;  // matches enqueue_forward
 
   // Attention work list: one item per 64-row block of (token, q-head) rows;
   // when the blocks cannot fill the GPU, long key ranges are split
@@ -472,16 +480,17 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   std::vector<Blk> blks;
   for (int i = 0; i < n; ++i) {
     const int L = mh_.q_len[i], H = mh_.hist[i];
-    for (int r0 = 0; r0 < L * G; r0 += kAttnRows) {
-      const int p_hi = H + std::min(r0 + kAttnRows - 1, L * G - 1) / G;
+    for (int r0 = 0; r0 < L * G; r0 += attn_rows) {
+      const int p_hi = H + std::min(r0 + attn_rows - 1, L * G - 1) / G;
       blks.push_back({i, r0, (p_hi + 1 + kPage - 1) / kPage});
     }
   }
   std::stable_sort(blks.begin(), blks.end(), [](const Blk& a, const Blk& b) { return a.need > b.need; });
   constexpr int kMinSplitTiles = 8;
   const int base = static_cast<int>(blks.size());
-  const int ctas = base * m_.n_kv_heads, target = 2 * num_sms();
-  const int f = ctas < target ? (target + ctas - 1) / ctas : 1;
+  // One wave for the tcgen05 kernel (one CTA per SM), two for the warp-MMA one.
+  const int ctas = base * m_.n_kv_heads, target = (attn_rows == kAttnTcRows ? 1 : 2) * num_sms();
+  const int f = std::min(32, ctas < target ? (target + ctas - 1) / ctas : 1);  // combine: <= 32 splits
   int nw = 0, nc = 0, n_items = base;
   std::vector<Blk> full;
   for (const Blk& b : blks) {
@@ -525,7 +534,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
     lp_check(cudaGraphLaunch(it->second, stream_), "graph launch");
   } else {
     // Standard / packed / uncaptured: eager launch sized to the live batch.
-    enqueue_forward(t_cap, r_cap, stream_);
+    enqueue_forward(t_cap, r_cap, stream_, false);
   }
   lp_check(cudaGetLastError(), "forward launch");
   lp_check(cudaEventRecord(ev_end_, stream_), "event");

@@ -91,7 +91,7 @@ class Instance {
   void alloc_weights();
   void alloc_arena();
   SplitPlan plan_for(int t_cap, int r_cap) const;
-  void enqueue_forward(int t_cap, int r_cap, cudaStream_t st);
+  void enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph);
   const CUtensorMap& act_map(const bf16* buf, int rows, int cols, int box_rows);
   void gemm(const CUtensorMap& tm_w, const GemmPlan& p, GemmArgs g, const bf16* x, int x_rows, cudaStream_t st);
   std::vector<int32_t> alloc_pages(int n);
@@ -142,6 +142,10 @@ class Instance {
   // Fused GEMM epilogues (QKV bias+RoPE+KV append, residual add) when the
   // plan has no split-K; LP_FUSE_EPI=0 disables them (A/B measurements).
   bool fuse_epilogues_ = true;
+  // head_dim 128 attention on the tcgen05/TMEM kernel (128-row work items);
+  // LP_ATTN_TC=0 selects the warp-MMA kernel (64-row items) instead.
+  bool attn_tc_ = true;
+  int attn_rows_ = kAttnRows;
 
   // graphs
   std::map<int64_t, cudaGraphExec_t> graphs_;
