@@ -39,31 +39,45 @@ int pow2_bn(int t) {
   return b;
 }
 
-// bn: smallest power-of-two tile >= tokens (<= 256). CTA pairs
-// (cta_group::2) once the token tile is >= 128 wide: the activation tile is
-// then re-read per 256 weight rows instead of per 128. Split-K only when the
-// (m, n) tiles cannot occupy every SM (pair) and only for fp32-partial outputs.
-GemmPlan plan_gemm(int M, int K, int t_cap, bool allow_split, int sms) {
-  GemmPlan p;
-  p.bn = pow2_bn(std::min(t_cap, 256));
-  p.pair = (p.bn >= 128 && M % 256 == 0) ? 2 : 1;
-  const int workers = sms / p.pair;
-  const int units = (M / (128 * p.pair)) * ((t_cap + p.bn - 1) / p.bn);
-  if (!allow_split) return p;
-  // Split-K factor minimising wave quantisation: time ~ ceil(units*S/workers)/S
-  // per unit of work, with a small charge per extra split for the fp32
-  // partial round trip; at least 4 k-blocks per split, and S*T bounded so the
-  // partials stay a small fraction of the weight stream.
-  const int s_max = std::max(1, std::min({8, (K / 64) / 4, std::max(1, 4096 / t_cap)}));
+// Largest split-K factor a launch capacity allows: >= 4 k-blocks per split,
+// S * t_cap <= 8192 rows of fp32 partials (workspace bound), S <= 8.
+int split_cap(int K, int t_cap) { return std::max(1, std::min({8, (K / 64) / 4, std::max(1, 8192 / t_cap)})); }
+
+}  // namespace
+
+// Split-K factor minimising wave quantisation for the LIVE token count:
+// time ~ ceil(units*S/workers)/S per unit of work, with a small charge per
+// extra split for the fp32 partial round trip.
+int choose_splits(int M, int bn, int pair, int n_live, int s_cap, int sms) {
+  const int workers = sms / pair;
+  const int units = (M / (128 * pair)) * std::max(1, (n_live + bn - 1) / bn);
+  int best_s = 1;
   double best = 1e30;
-  for (int s = 1; s <= s_max; ++s) {
+  for (int s = 1; s <= s_cap; ++s) {
     const double waves = static_cast<double>((units * s + workers - 1) / workers);
     const double cost = waves / s * (1.0 + 0.03 * (s - 1));
     if (cost < best - 1e-9) {
       best = cost;
-      p.splits = s;
+      best_s = s;
     }
   }
+  return best_s;
+}
+
+namespace {
+
+// bn: smallest power-of-two tile >= tokens (<= 256). CTA pairs
+// (cta_group::2) once the token tile is >= 128 wide: the activation tile is
+// then re-read per 256 weight rows instead of per 128. Split-K (fp32-partial
+// outputs only) is chosen per batch from the live token count at submit time
+// (device metadata); `splits` here is the choice at full capacity.
+GemmPlan plan_gemm(int M, int K, int t_cap, bool allow_split, int sms) {
+  GemmPlan p;
+  p.bn = pow2_bn(std::min(t_cap, 256));
+  p.pair = (p.bn >= 128 && M % 256 == 0) ? 2 : 1;
+  if (!allow_split) return p;
+  p.s_cap = split_cap(K, t_cap);
+  p.splits = choose_splits(M, p.bn, p.pair, t_cap, p.s_cap, sms);
   return p;
 }
 
@@ -79,7 +93,7 @@ Instance::Instance(const lp_model_desc& m, const lp_instance_desc& d) : m_(m), d
   d_.page_size = kPage;
   if (d_.max_tokens <= 0) d_.max_tokens = 16384;
   if (d_.max_members <= 0) d_.max_members = 64;
-  if (const char* e = std::getenv("LP_FUSE_EPI"); e && e[0] == '0') fuse_epilogues_ = false;
+  if (const char* e = std::getenv("LP_FUSE_EPI"); e && e[0] == '1') fuse_epilogues_ = true;
   if (const char* e = std::getenv("LP_ATTN_TC"); e && e[0] == '0') attn_tc_ = false;
   lp_check(cudaSetDevice(d.device), "cudaSetDevice");
   lp_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
@@ -175,8 +189,8 @@ void Instance::alloc_arena() {
   ws_elems_ = 0;
   for (int t = 16; t <= t_max_; t += 16) {
     const SplitPlan p = plan_for(t, 1);
-    const size_t mx = std::max<size_t>({size_t(p.qkv.splits) * qkv_out, size_t(p.o.splits) * h,
-                                        size_t(p.d.splits) * h});
+    const size_t mx = std::max<size_t>({size_t(p.qkv.s_cap) * qkv_out, size_t(p.o.s_cap) * h,
+                                        size_t(p.d.s_cap) * h});
     ws_elems_ = std::max(ws_elems_, mx * size_t(t));
   }
   ws_ = dmalloc<float>(ws_elems_, allocs_);
@@ -277,7 +291,8 @@ const CUtensorMap& Instance::act_map(const bf16* buf, int rows, int cols, int bo
 
 void Instance::gemm(const CUtensorMap& tm_w, const GemmPlan& p, GemmArgs g, const bf16* x, int x_rows,
                     cudaStream_t st) {
-  g.splits = p.splits;
+  // With a device-side split count the grid is sized for the largest one allowed.
+  g.splits = g.splits_dev ? p.s_cap : p.splits;
   gemm_launch(tm_w, act_map(x, x_rows, g.K, gemm_b_box_rows(p.bn, p.pair)), g, p.bn, st, 0, p.pair);
 }
 
@@ -310,8 +325,9 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
       g.qkv = QkvEpi{md_.positions, md_.slots, inv_freq_, q_, kv_layer, nq, nkv, kPage};
       gemm(w.tm_qkv, p.qkv, g, x_norm_, t_max_, st);
     } else {
+      g.splits_dev = md_.scalars + 4;  // per-batch split-K (submit)
       gemm(w.tm_qkv, p.qkv, g, x_norm_, t_max_, st);
-      QkvCtx qc{n_tok, t_cap, nq, nkv, D, kPage, ws_, p.qkv.splits, size_t(t_cap), w.bqkv,
+      QkvCtx qc{n_tok, t_cap, nq, nkv, D, kPage, ws_, p.qkv.splits, md_.scalars + 4, size_t(t_cap), w.bqkv,
                 md_.positions, md_.slots, inv_freq_, q_, kv_layer};
       qkv_post(qc, st);
     }
@@ -328,9 +344,11 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
     if (o_fused) {  // residual add in the epilogue; the norm kernel then reads x_resid only
       g.mode = kEpiResidAdd;
       g.resid = x_resid_;
+    } else {
+      g.splits_dev = md_.scalars + 5;
     }
     gemm(w.tm_o, p.o, g, attn_, t_max_, st);
-    resid_rmsnorm(rc, ws_, o_fused ? 0 : p.o.splits, t_cap, x_resid_, w.g_mlp, x_norm_, st);
+    resid_rmsnorm(rc, ws_, 0, o_fused ? nullptr : md_.scalars + 5, t_cap, x_resid_, w.g_mlp, x_norm_, st);
     // gate/up with fused SiLU*up.
     g = GemmArgs{};
     g.M = 2 * I; g.N = t_cap; g.K = h; g.n_dev = n_tok;
@@ -344,10 +362,12 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
     if (d_fused) {
       g.mode = kEpiResidAdd;
       g.resid = x_resid_;
+    } else {
+      g.splits_dev = md_.scalars + 6;
     }
     gemm(w.tm_d, p.d, g, act_, t_max_, st);
     const bf16* g_next = (l + 1 < m_.layers) ? layers_[l + 1].g_attn : g_final_;
-    resid_rmsnorm(rc, ws_, d_fused ? 0 : p.d.splits, t_cap, x_resid_, g_next, x_norm_, st);
+    resid_rmsnorm(rc, ws_, 0, d_fused ? nullptr : md_.scalars + 6, t_cap, x_resid_, g_next, x_norm_, st);
   }
   // Final norm already applied; LM head on the last real token per member.
   gather_rows(n_mem, r_cap, md_.last_idx, x_norm_, x_last_, h, next_keys_, st);
@@ -509,13 +529,25 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   mh_.scalars[1] = n;
   mh_.scalars[2] = nw;
   mh_.scalars[3] = nc;
+  // Split-K per projection for the live token count (fused epilogues need 1).
+  {
+    const SplitPlan sp = plan_for(t_cap, r_cap);
+    const int h = m_.hidden, D = m_.head_dim, sms = num_sms();
+    const int qkv_out = (m_.n_q_heads + 2 * m_.n_kv_heads) * D;
+    auto live_s = [&](const GemmPlan& gp, int M, bool fused) {
+      return fused ? 1 : choose_splits(M, gp.bn, gp.pair, t, gp.s_cap, sms);
+    };
+    mh_.scalars[4] = live_s(sp.qkv, qkv_out, fuse_epilogues_ && sp.qkv.splits == 1 && D == 128);
+    mh_.scalars[5] = live_s(sp.o, h, fuse_epilogues_ && sp.o.splits == 1);
+    mh_.scalars[6] = live_s(sp.d, h, fuse_epilogues_ && sp.d.splits == 1);
+  }
 
   last_h2d_bytes_ = 0;
   auto h2d = [&](void* dst, const void* src, size_t bytes) {
     if (bytes) lp_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_), "meta h2d");
     last_h2d_bytes_ += bytes;
   };
-  h2d(md_.scalars, mh_.scalars, 16);
+  h2d(md_.scalars, mh_.scalars, 32);
   h2d(md_.tokens, mh_.tokens, size_t(t) * 4);
   h2d(md_.positions, mh_.positions, size_t(t) * 4);
   h2d(md_.slots, mh_.slots, size_t(t) * 4);
@@ -570,10 +602,6 @@ double Instance::time_gemm(int layer, int which, int t_cap, int n_live, int iter
   const SplitPlan sp = plan_for(t_cap, std::min(t_cap, r_max_));
   const LayerW& w = layers_[layer];
   if (submitted_) lp_check(cudaEventSynchronize(ev_h2d_), "staging reuse");
-  mh_.scalars[0] = n_live;
-  mh_.scalars[1] = std::min(n_live, r_max_);
-  lp_check(cudaMemcpyAsync(md_.scalars, mh_.scalars, 16, cudaMemcpyHostToDevice, stream_), "meta");
-  lp_check(cudaStreamSynchronize(stream_), "sync");
   GemmArgs g;
   g.N = t_cap;
   g.n_dev = md_.scalars;
@@ -589,6 +617,13 @@ double Instance::time_gemm(int layer, int which, int t_cap, int n_live, int iter
     case 3: g.M = h; g.K = I; g.mode = kEpiF32Partial; tm = &w.tm_d; p = &sp.d; x = act_; break;
     default: throw ShapeMismatch("time_gemm: which in 0..3");
   }
+  // Same per-batch split-K choice as a forward with n_live tokens.
+  mh_.scalars[0] = n_live;
+  mh_.scalars[1] = std::min(n_live, r_max_);
+  mh_.scalars[4] = choose_splits(g.M, p->bn, p->pair, n_live, p->s_cap, num_sms());
+  if (g.mode == kEpiF32Partial) g.splits_dev = md_.scalars + 4;
+  lp_check(cudaMemcpyAsync(md_.scalars, mh_.scalars, 32, cudaMemcpyHostToDevice, stream_), "meta");
+  lp_check(cudaStreamSynchronize(stream_), "sync");
   // Realistic operand values (unit-variance activations): an all-zero input
   // would under-state power draw and over-state the clock.
   init_weights(const_cast<bf16*>(x), size_t(t_cap) * g.K, 77, 999, std::sqrt(3.0f) / 8388608.0f, 0, g.K,

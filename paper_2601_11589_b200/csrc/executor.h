@@ -59,8 +59,10 @@ struct Meta {
 struct GemmPlan {
   int bn = 16;     // token tile
   int pair = 1;    // 2 = cta_group::2 CTA pair
-  int splits = 1;  // split-K factor (fp32 partial epilogues only)
+  int splits = 1;  // split-K factor at full capacity (fp32 partial epilogues only)
+  int s_cap = 1;   // largest split-K factor the workspace allows at this capacity
 };
+int choose_splits(int M, int bn, int pair, int n_live, int s_cap, int sms);
 struct SplitPlan {
   GemmPlan qkv, o, gu, d, lm;
 };
@@ -139,9 +141,11 @@ class Instance {
   std::map<std::tuple<const void*, int, int>, CUtensorMap> act_maps_;
 
   cudaEvent_t timers_[kTimerSlots] = {};
-  // Fused GEMM epilogues (QKV bias+RoPE+KV append, residual add) when the
-  // plan has no split-K; LP_FUSE_EPI=0 disables them (A/B measurements).
-  bool fuse_epilogues_ = true;
+  // Fused GEMM epilogues (QKV bias+RoPE+KV append, residual add) for GEMMs
+  // whose capacity plan has no split-K. Measured neutral against the split
+  // reduction kernels, and they pin the runtime split-K to 1, so they are
+  // opt-in (LP_FUSE_EPI=1); the default chooses split-K per batch.
+  bool fuse_epilogues_ = false;
   // head_dim 128 attention on the tcgen05/TMEM kernel (128-row work items);
   // LP_ATTN_TC=0 selects the warp-MMA kernel (64-row items) instead.
   bool attn_tc_ = true;

@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int m_tiles = args.M / (kBM * kPair);   // tiles of this variant (128 or 256 rows)
   const int n_tiles = (args.N + BN - 1) / BN;
   const int num_kb = args.K / kBK;
-  const int splits = args.splits;
+  // Split-K factor: from device metadata when the plan is chosen per batch (pre-graph H2D).
+  const int splits = args.splits_dev ? max(1, *args.splits_dev) : args.splits;
   const int units = splits * m_tiles * n_tiles;
   const int worker = blockIdx.x / kPair;        // CTA (pair) index
   const int n_workers = gridDim.x / kPair;

@@ -43,6 +43,7 @@ struct GemmArgs {
   int N = 0;            // token capacity (rows of X)
   int K = 0;            // reduction length (multiple of 64)
   int splits = 1;       // split-K factor
+  const int* splits_dev = nullptr;  // optional device-side split-K factor (overrides `splits`)
   const int* n_dev = nullptr;  // optional device-side live token count (<= N)
   int mode = kEpiBf16;
   void* out = nullptr;

@@ -75,13 +75,14 @@ __global__ void __launch_bounds__(kRowThreads)
 // x_resid += sum of split partials; x_norm = bf16(rmsnorm(x_resid) * gamma).
 // All of a thread's loads (residual + every split) are issued before use.
 __global__ void __launch_bounds__(kRowThreads)
-    resid_rmsnorm_kernel(RowCtx c, const float* __restrict__ ws, int splits, size_t ws_stride_rows,
-                         float* __restrict__ x_resid, const bf16* __restrict__ gamma,
+    resid_rmsnorm_kernel(RowCtx c, const float* __restrict__ ws, int splits, const int* splits_dev,
+                         size_t ws_stride_rows, float* __restrict__ x_resid, const bf16* __restrict__ gamma,
                          bf16* __restrict__ x_norm) {
   __shared__ float red[33];
   pdl_trigger();
   const int t = blockIdx.x;
   const bool live = t < *c.n_live;
+  if (splits_dev) splits = *splits_dev;  // pre-graph H2D metadata
   pdl_wait();
   if (!live) return;
   const int h4 = c.h / 4;
@@ -143,10 +144,11 @@ __global__ void __launch_bounds__(kQkvThreads) qkv_post_kernel(QkvCtx c) {
   const int head = j / half, i = j % half;
   const int c0 = head * c.d + i, c1 = c0 + half;
   float x0 = __bfloat162float(c.bias[c0]), x1 = __bfloat162float(c.bias[c1]);
+  const int splits = c.splits_dev ? *c.splits_dev : c.splits;
   float p0[8], p1[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    if (s < c.splits) {
+    if (s < splits) {
       const float* row = c.ws + (static_cast<size_t>(s) * c.ws_stride_rows + t) * qkv_out;
       p0[s] = row[c0];
       p1[s] = row[c1];
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(kQkvThreads) qkv_post_kernel(QkvCtx c) {
   }
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    if (s < c.splits) {
+    if (s < splits) {
       x0 += p0[s];
       x1 += p1[s];
     }
@@ -257,10 +259,10 @@ void embed_rmsnorm(const RowCtx& c, const int* tokens, const bf16* embed, const 
            x_resid, x_norm);
 }
 
-void resid_rmsnorm(const RowCtx& c, const float* ws, int splits, size_t ws_stride_rows,
+void resid_rmsnorm(const RowCtx& c, const float* ws, int splits, const int* splits_dev, size_t ws_stride_rows,
                    float* x_resid, const bf16* gamma, bf16* x_norm, cudaStream_t st) {
-  launch_k(resid_rmsnorm_kernel, dim3(c.t_cap), dim3(kRowThreads), 0, st, c, ws, splits, ws_stride_rows,
-           x_resid, gamma, x_norm);
+  launch_k(resid_rmsnorm_kernel, dim3(c.t_cap), dim3(kRowThreads), 0, st, c, ws, splits, splits_dev,
+           ws_stride_rows, x_resid, gamma, x_norm);
 }
 
 void qkv_post(const QkvCtx& c, cudaStream_t st) {

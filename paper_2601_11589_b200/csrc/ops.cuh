@@ -31,7 +31,8 @@ void embed_rmsnorm(const RowCtx& c, const int* tokens, const bf16* embed, const 
                    float* x_resid, bf16* x_norm, cudaStream_t st);
 
 // x_resid[t] += sum_s ws[s][t]; x_norm[t] = bf16(rmsnorm(x_resid[t]) * gamma)
-void resid_rmsnorm(const RowCtx& c, const float* ws, int splits, size_t ws_stride_rows,
+// splits_dev (optional): device-side split count overriding `splits`.
+void resid_rmsnorm(const RowCtx& c, const float* ws, int splits, const int* splits_dev, size_t ws_stride_rows,
                    float* x_resid, const bf16* gamma, bf16* x_norm, cudaStream_t st);
 
 struct QkvCtx {
@@ -41,6 +42,7 @@ struct QkvCtx {
   int page_size;
   const float* ws;           // [splits][t_cap][qkv_out] fp32 partials
   int splits;
+  const int* splits_dev;     // optional device-side split count (overrides `splits`)
   size_t ws_stride_rows;
   const bf16* bias;          // [qkv_out]
   const int* positions;      // [T] absolute position
