@@ -135,11 +135,21 @@ def dist_env():
     return ws, rank, local
 
 
+def gpu_of(local: int) -> int:
+    """GPU of this rank. LP_BENCH_SHARE_GPU=1 maps every rank to GPU 0 (a
+    functional check of the multi-rank path on a one-GPU box; not a
+    measurement)."""
+    return 0 if os.environ.get("LP_BENCH_SHARE_GPU") == "1" else local
+
+
 def dist_init(ws: int, local: int):
     if ws <= 1:
         return None
     import torch
     import torch.distributed as dist
+    if os.environ.get("LP_BENCH_SHARE_GPU") == "1":
+        dist.init_process_group("gloo")  # NCCL refuses two ranks on one device
+        return dist
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return dist
@@ -321,7 +331,9 @@ def run_ours(args) -> None:
     model = QWEN25_7B
     peaks = load_peaks()
 
-    inst = PrefillInstance(model, device=local, max_tokens=16384, max_members=64)
+    # Short-only stream: every session is released after its single turn, so a
+    # 4096-page pool (262K tokens, 14.7 GB at 7B) is ample and leaves HBM headroom.
+    inst = PrefillInstance(model, device=gpu_of(local), max_tokens=16384, max_members=64, kv_pages=4096)
     inst.capture_graphs()  # 6 lengths x 7 depths (GraphGrid defaults)
 
     # ---- Phase A: live engine run (real GPU service times drive the clock)
@@ -365,7 +377,7 @@ def run_ours(args) -> None:
     reqs = 0
     import torch
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ selects this region
-    with ClockSampler(local) as clk:
+    with ClockSampler(gpu_of(local)) as clk:
         inst.timer_record(0)
         for j in range(args.steps):
             i = args.warmup + j
