@@ -266,7 +266,11 @@ int Instance::combine_cap_for(int t_cap, int r_cap) const {
   return std::min(c_max_, (t_cap * G + kAttnRows - 1) / kAttnRows + r_cap);
 }
 int Instance::work_cap_for(int t_cap, int r_cap) const {
-  return std::min(w_max_, combine_cap_for(t_cap, r_cap) + kAttnSplitExtra);
+  // Splits only ever target ~2 waves of (items x kv heads) CTAs, so the extra
+  // room is 2 * SMs / nkv items (early-exit CTAs beyond the live count still
+  // occupy SM slots and would delay the next GEMM's PDL weight prefetch).
+  const int extra = std::min(kAttnSplitExtra, (2 * num_sms() + m_.n_kv_heads - 1) / m_.n_kv_heads);
+  return std::min(w_max_, combine_cap_for(t_cap, r_cap) + extra);
 }
 
 SplitPlan Instance::plan_for(int t_cap, int r_cap) const {
