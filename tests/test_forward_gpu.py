@@ -165,3 +165,29 @@ def test_fused_epilogues_match_unfused(monkeypatch):
     want = oracle.forward([(m.session_id, m.new_tokens, m.history) for m in members], toks)
     d = (logits["1"] - want).abs()
     assert d.max().item() <= 5e-2 and d.mean().item() <= 1e-2
+
+
+def test_long_history_split_kv():
+    """Short re-prefills over long histories: the key range is split across
+    CTAs (flash-decoding style) and merged by the combine kernel — on the
+    warp-MMA kernel (tiny model, graph shape) and on the tcgen05 kernel
+    (7B-shaped, eager packed batch)."""
+    # tiny: 2000-token history, then a 20-token re-prefill through a graph
+    inst = PrefillInstance(TINY, max_tokens=4096, max_members=8, kv_pages=256)
+    inst.capture_graphs(lengths=(32,), depths=(2,))
+    oracle = FO.OracleModel(FO.TINY)
+    pages = PageOracle(256)
+    _compare(inst, oracle, pages, 0, 0, KIND_PACKED, [Member(0, 1, 2000, 0)])
+    _compare(inst, oracle, pages, 32, 2, KIND_GRAPH, [Member(1, 1, 20, 2000), Member(2, 2, 30, 0)])
+    _kv_check(inst, oracle, 1, [0, 1])
+    inst.close()
+    # 7B-shaped, 2 layers: 1500-token history + a 64-token chunk (eager -> tcgen05 kernel)
+    from paper_2601_11589_b200.instance import QWEN25_7B
+    cfg = QWEN25_7B.with_layers(2)
+    inst = PrefillInstance(cfg, max_tokens=2048, max_members=8, kv_pages=64, use_graphs=False)
+    oracle = FO.OracleModel(FO.with_layers(FO.QWEN25_7B, 2))
+    pages = PageOracle(64)
+    tol = (5e-2, 1e-2, 0.9999)
+    _compare(inst, oracle, pages, 0, 0, KIND_PACKED, [Member(0, 5, 1500, 0)], tol=tol)
+    _compare(inst, oracle, pages, 0, 0, KIND_PACKED, [Member(1, 5, 64, 1500), Member(2, 6, 16, 0)], tol=tol)
+    inst.close()
