@@ -333,6 +333,7 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
       gemm(w.tm_qkv, p.qkv, g, x_norm_, t_max_, st);
       QkvCtx qc{n_tok, t_cap, nq, nkv, D, kPage, ws_, p.qkv.splits, md_.scalars + 4, size_t(t_cap), w.bqkv,
                 md_.positions, md_.slots, inv_freq_, q_, kv_layer};
+      qc.s_cap = p.qkv.s_cap;
       qkv_post(qc, st);
     }
     AttnCtx ac{md_.scalars + 2, md_.work, md_.scalars + 3, md_.combine, md_.q_start, md_.q_len, md_.hist,

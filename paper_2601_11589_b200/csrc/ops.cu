@@ -1,4 +1,6 @@
+#include <algorithm>
 #include <cstdio>
+#include <stdexcept>
 
 #include "launch.cuh"
 #include "ops.cuh"
@@ -128,62 +130,121 @@ __global__ void __launch_bounds__(kRowThreads)
   }
 }
 
-// grid (token, pair block); one thread per rotary pair (j, j + d/2) of one head.
-constexpr int kQkvThreads = 128;
-__global__ void __launch_bounds__(kQkvThreads) qkv_post_kernel(QkvCtx c) {
+// One CTA per token. A "unit" is 4 consecutive rotary pairs of one head:
+// columns j..j+3 and j+d/2..j+d/2+3 (two float4 per split). Thread u owns
+// units u, u + blockDim, ... (<= U), so a warp reads 2 x 256 B contiguous
+// runs per load instruction. The d/2 rotary angles of the token are computed
+// once into shared memory (q and k heads share them). Loads of U units x SU
+// splits are issued before any add: U=4, SU=1 for large token counts (split-K
+// <= 2, many CTAs per SM), U=1, SU=8 for short batches (deep split-K, few
+// CTAs: all partials of a unit in flight at once).
+constexpr int kQkvMaxHalf = 128;  // head_dim <= 256
+__device__ __forceinline__ void add4(float4& a, const float4 b) {
+  a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+}
+__device__ __forceinline__ float4 bf4(const bf16* p) {
+  const uint2 r = *reinterpret_cast<const uint2*>(p);
+  const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.x));
+  const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.y));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+__device__ __forceinline__ void st_bf4(bf16* p, float a, float b, float c, float d) {
+  const __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 r;
+  r.x = *reinterpret_cast<const uint32_t*>(&lo);
+  r.y = *reinterpret_cast<const uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(p) = r;
+}
+template <int U, int SU>
+__global__ void qkv_post_kernel(QkvCtx c) {
+  __shared__ float s_cos[kQkvMaxHalf], s_sin[kQkvMaxHalf];
   pdl_trigger();
   const int t = blockIdx.x;
-  const bool live = t < *c.n_live;
-  pdl_wait();
-  if (!live) return;
-  const int half = c.d / 2;
-  const int total = (c.nq + 2 * c.nkv) * half;
-  const int j = blockIdx.y * kQkvThreads + threadIdx.x;
-  if (j >= total) return;
-  const int qkv_out = (c.nq + 2 * c.nkv) * c.d;
-  const int head = j / half, i = j % half;
-  const int c0 = head * c.d + i, c1 = c0 + half;
-  float x0 = __bfloat162float(c.bias[c0]), x1 = __bfloat162float(c.bias[c1]);
-  const int splits = c.splits_dev ? *c.splits_dev : c.splits;
-  float p0[8], p1[8];
+  if (t >= *c.n_live) {
+    pdl_wait();
+    return;
+  }
+  const int half = c.d / 2, upr = half / 4;  // units per head
+  const int heads = c.nq + 2 * c.nkv;
+  const int units = heads * upr;
+  const int qkv_out = heads * c.d;
+  // bias and rotary table: host-written metadata / static weights, safe before the wait
+  float4 x0[U], x1[U];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    if (s < splits) {
-      const float* row = c.ws + (static_cast<size_t>(s) * c.ws_stride_rows + t) * qkv_out;
-      p0[s] = row[c0];
-      p1[s] = row[c1];
+  for (int k = 0; k < U; ++k) {
+    const int u = threadIdx.x + k * blockDim.x;
+    if (u < units) {
+      const int c0 = (u / upr) * c.d + (u % upr) * 4;
+      x0[k] = bf4(c.bias + c0);
+      x1[k] = bf4(c.bias + c0 + half);
     }
   }
-#pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    if (s < splits) {
-      x0 += p0[s];
-      x1 += p1[s];
-    }
-  }
-  if (head < c.nq + c.nkv) {  // RoPE on q and k heads (rotate-half pairing)
+  if (threadIdx.x < half) {
     float sn, cs;
-    sincosf(static_cast<float>(c.positions[t]) * c.inv_freq[i], &sn, &cs);
-    const float r0 = x0 * cs - x1 * sn;
-    const float r1 = x1 * cs + x0 * sn;
-    x0 = r0;
-    x1 = r1;
+    sincosf(static_cast<float>(c.positions[t]) * c.inv_freq[threadIdx.x], &sn, &cs);
+    s_cos[threadIdx.x] = cs;
+    s_sin[threadIdx.x] = sn;
   }
-  const bf16 b0 = __float2bfloat16_rn(x0), b1 = __float2bfloat16_rn(x1);
-  if (head < c.nq) {
-    bf16* q = c.q_out + static_cast<size_t>(t) * c.nq * c.d + head * c.d;
-    q[i] = b0;
-    q[i + half] = b1;
-  } else {
-    const int slot = c.slot_mapping[t];
-    const int page = slot / c.page_size, s_in = slot % c.page_size;
-    const size_t page_elems = static_cast<size_t>(2) * c.nkv * c.page_size * c.d;
-    const bool is_v = head >= c.nq + c.nkv;
-    const int g = is_v ? head - c.nq - c.nkv : head - c.nq;
-    bf16* dst = c.kv_layer + page * page_elems +
-                ((static_cast<size_t>(is_v ? 1 : 0) * c.nkv + g) * c.page_size + s_in) * c.d;
-    dst[i] = b0;
-    dst[i + half] = b1;
+  pdl_wait();
+  const int splits = c.splits_dev ? max(1, *c.splits_dev) : c.splits;
+  for (int s0 = 0; s0 < splits; s0 += SU) {
+    float4 p0[SU][U], p1[SU][U];
+#pragma unroll
+    for (int e = 0; e < SU; ++e) {
+      const float* row = c.ws + (static_cast<size_t>(s0 + e) * c.ws_stride_rows + t) * qkv_out;
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int u = threadIdx.x + k * blockDim.x;
+        if (u < units && s0 + e < splits) {
+          const int c0 = (u / upr) * c.d + (u % upr) * 4;
+          p0[e][k] = *reinterpret_cast<const float4*>(row + c0);
+          p1[e][k] = *reinterpret_cast<const float4*>(row + c0 + half);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < SU; ++e) {
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if (threadIdx.x + k * blockDim.x < units && s0 + e < splits) {
+          add4(x0[k], p0[e][k]);
+          add4(x1[k], p1[e][k]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int slot = c.slot_mapping[t];
+  const int page = slot / c.page_size, s_in = slot % c.page_size;
+  const size_t page_elems = static_cast<size_t>(2) * c.nkv * c.page_size * c.d;
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    const int u = threadIdx.x + k * blockDim.x;
+    if (u >= units) continue;
+    const int head = u / upr, j = (u % upr) * 4;
+    float a[4] = {x0[k].x, x0[k].y, x0[k].z, x0[k].w};
+    float b[4] = {x1[k].x, x1[k].y, x1[k].z, x1[k].w};
+    if (head < c.nq + c.nkv) {  // RoPE on q and k heads (rotate-half pairing)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float cs = s_cos[j + e], sn = s_sin[j + e];
+        const float r0 = a[e] * cs - b[e] * sn;
+        const float r1 = b[e] * cs + a[e] * sn;
+        a[e] = r0;
+        b[e] = r1;
+      }
+    }
+    bf16* dst;
+    if (head < c.nq) {
+      dst = c.q_out + static_cast<size_t>(t) * c.nq * c.d + head * c.d;
+    } else {
+      const bool is_v = head >= c.nq + c.nkv;
+      const int g = is_v ? head - c.nq - c.nkv : head - c.nq;
+      dst = c.kv_layer + page * page_elems +
+            ((static_cast<size_t>(is_v ? 1 : 0) * c.nkv + g) * c.page_size + s_in) * c.d;
+    }
+    st_bf4(dst + j, a[0], a[1], a[2], a[3]);
+    st_bf4(dst + j + half, b[0], b[1], b[2], b[3]);
   }
 }
 
@@ -266,9 +327,18 @@ void resid_rmsnorm(const RowCtx& c, const float* ws, int splits, const int* spli
 }
 
 void qkv_post(const QkvCtx& c, cudaStream_t st) {
-  const int pairs = (c.nq + 2 * c.nkv) * (c.d / 2);
-  launch_k(qkv_post_kernel, dim3(c.t_cap, (pairs + kQkvThreads - 1) / kQkvThreads), dim3(kQkvThreads), 0,
-           st, c);
+  const int half = c.d / 2;
+  if (half % 4 != 0 || half > kQkvMaxHalf)
+    throw std::runtime_error("qkv_post: head_dim must be a multiple of 8 and <= 256");
+  const int units = (c.nq + 2 * c.nkv) * (half / 4);
+  const bool deep = c.s_cap > 2 && units <= 1024;
+  const int per = deep ? 1 : 4;
+  const int threads = std::max(((units + per - 1) / per + 31) / 32 * 32, half);
+  if (threads > 1024) throw std::runtime_error("qkv_post: too many heads for one CTA per token");
+  if (deep)
+    launch_k(qkv_post_kernel<1, 8>, dim3(c.t_cap), dim3(threads), 0, st, c);
+  else
+    launch_k(qkv_post_kernel<4, 1>, dim3(c.t_cap), dim3(threads), 0, st, c);
 }
 
 void gather_rows(const int* n_rows, int r_cap, const int* idx, const bf16* src, bf16* dst, int h,

@@ -50,6 +50,7 @@ struct QkvCtx {
   const float* inv_freq;     // [d/2]
   bf16* q_out;               // [T, nq*d]
   bf16* kv_layer;            // layer base of the paged cache
+  int s_cap = 8;             // upper bound of the split count (picks the load schedule)
 };
 // reduce splits + bias; RoPE(q, k); q -> q_out; k, v -> paged cache
 void qkv_post(const QkvCtx& c, cudaStream_t st);
