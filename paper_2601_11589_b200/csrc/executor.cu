@@ -108,6 +108,7 @@ Instance::~Instance() {
   cudaSetDevice(d_.device);
   cudaStreamSynchronize(stream_);
   for (auto& [k, g] : graphs_) cudaGraphExecDestroy(g);
+  for (auto& [k, g] : chunk_graphs_) cudaGraphExecDestroy(g);
   for (void* p : allocs_) cudaFree(p);
   if (meta_host_) cudaFreeHost(meta_host_);
   cudaEventDestroy(ev_start_);
@@ -418,18 +419,24 @@ void Instance::capture_graphs(const std::vector<int64_t>& lens, const std::vecto
       if (t_cap > t_max_ || dep > r_max_) continue;
       const int64_t key = graph_key(L, dep);
       if (graphs_.count(key)) continue;
-      enqueue_forward(static_cast<int>(t_cap), dep, stream_, true);  // warm-up (no live work)
-      cudaGraph_t graph;
-      lp_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
-      enqueue_forward(static_cast<int>(t_cap), dep, stream_, true);
-      lp_check(cudaStreamEndCapture(stream_, &graph), "end capture");
-      cudaGraphExec_t exec;
-      lp_check(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
-      cudaGraphDestroy(graph);
-      graphs_[key] = exec;
+      graphs_[key] = capture_one(static_cast<int>(t_cap), dep, true);
     }
   }
+  for (int t_cap = kChunkGraphStep; t_cap <= std::min(kChunkGraphMax, t_max_); t_cap += kChunkGraphStep)
+    if (!chunk_graphs_.count(t_cap)) chunk_graphs_[t_cap] = capture_one(t_cap, 1, false);
   lp_check(cudaStreamSynchronize(stream_), "capture sync");
+}
+
+cudaGraphExec_t Instance::capture_one(int t_cap, int r_cap, bool graph_attn) {
+  enqueue_forward(t_cap, r_cap, stream_, graph_attn);  // warm-up (no live work)
+  cudaGraph_t graph;
+  lp_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+  enqueue_forward(t_cap, r_cap, stream_, graph_attn);
+  lp_check(cudaStreamEndCapture(stream_, &graph), "end capture");
+  cudaGraphExec_t exec;
+  lp_check(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+  cudaGraphDestroy(graph);
+  return exec;
 }
 
 void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const int32_t* tokens) {
@@ -486,13 +493,29 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   }
 
   // Which launch runs this batch (fixes the attention grid capacity).
-  auto it = (shape.kind == LP_KIND_GRAPH && d_.use_graphs) ? graphs_.find(graph_key(shape.l_pad, shape.depth))
-                                                           : graphs_.end();
-  const int t_cap = it != graphs_.end() ? static_cast<int>(shape.l_pad * shape.depth)
-                                        : std::min(std::max(16, (t + 15) / 16 * 16), t_max_);
-  const int r_cap = it != graphs_.end() ? shape.depth : n;
+  // Grid-shape graph (warp-MMA attention), chunk graph for a one-member
+  // standard launch (tcgen05 attention), else eager sized to the live batch.
+  cudaGraphExec_t exec = nullptr;
+  int t_cap = std::min(std::max(16, (t + 15) / 16 * 16), t_max_);
+  int r_cap = n;
+  int attn_rows = attn_rows_;  // matches enqueue_forward
+  if (d_.use_graphs && shape.kind == LP_KIND_GRAPH) {
+    auto it = graphs_.find(graph_key(shape.l_pad, shape.depth));
+    if (it != graphs_.end()) {
+      exec = it->second;
+      t_cap = static_cast<int>(shape.l_pad * shape.depth);
+      r_cap = shape.depth;
+      attn_rows = kAttnRows;
+    }
+  } else if (d_.use_graphs && shape.kind == LP_KIND_STANDARD && n == 1) {
+    auto it = chunk_graphs_.find((t + kChunkGraphStep - 1) / kChunkGraphStep * kChunkGraphStep);
+    if (it != chunk_graphs_.end()) {
+      exec = it->second;
+      t_cap = it->first;
+      r_cap = 1;
+    }
+  }
   const int work_cap = work_cap_for(t_cap, r_cap);
-  const int attn_rows = it != graphs_.end() ? kAttnRows : attn_rows_;  // matches enqueue_forward
 
   // Attention work list: one item per 64-row block of (token, q-head) rows;
   // when the blocks cannot fill the GPU, long key ranges are split
@@ -511,7 +534,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
     }
   }
   std::stable_sort(blks.begin(), blks.end(), [](const Blk& a, const Blk& b) { return a.need > b.need; });
-  constexpr int kMinSplitTiles = 8;
+  constexpr int kMinSplitTiles = 2;
   const int base = static_cast<int>(blks.size());
   // One wave for the tcgen05 kernel (one CTA per SM), two for the warp-MMA one.
   const int ctas = base * m_.n_kv_heads, target = (attn_rows == kAttnTcRows ? 1 : 2) * num_sms();
@@ -567,8 +590,8 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
 
   lp_check(cudaEventRecord(ev_h2d_, stream_), "event");
   lp_check(cudaEventRecord(ev_start_, stream_), "event");
-  if (it != graphs_.end()) {
-    lp_check(cudaGraphLaunch(it->second, stream_), "graph launch");
+  if (exec) {
+    lp_check(cudaGraphLaunch(exec, stream_), "graph launch");
   } else {
     // Standard / packed / uncaptured: eager launch sized to the live batch.
     enqueue_forward(t_cap, r_cap, stream_, false);

@@ -153,6 +153,13 @@ class Instance {
 
   // graphs
   std::map<int64_t, cudaGraphExec_t> graphs_;
+  // Single-member standard launches (long-prefill chunks, scheduler.cpp:322-338)
+  // replay graphs captured per 64-token capacity up to kChunkGraphMax
+  // (= C_l, scheduler.hpp:46): an eager chunk forward is ~300 launches, which
+  // the host cannot issue as fast as the GPU retires them.
+  static constexpr int kChunkGraphStep = 64, kChunkGraphMax = 512;
+  std::map<int, cudaGraphExec_t> chunk_graphs_;
+  cudaGraphExec_t capture_one(int t_cap, int r_cap, bool graph_attn);
   bool submitted_ = false;
  public:
   size_t last_h2d_bytes_ = 0, last_d2h_bytes_ = 0;  // host<->device bytes of the last submit / read

@@ -73,7 +73,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // n_dev is written by the pre-graph H2D copy, never by a kernel: safe before pdl_wait.
   const int n_live = args.n_dev ? min(*args.n_dev, args.N) : args.N;
   const int m_tiles = args.M / (kBM * kPair);   // tiles of this variant (128 or 256 rows)
-  const int n_tiles = (args.N + BN - 1) / BN;
+  // Token tiles are sized from the LIVE token count: ceil(n_live / BN) tiles
+  // of equal width tw (a multiple of 16 <= BN), and each tile's MMA runs with
+  // N = its live width rounded up to 16 (the instruction descriptor is a
+  // runtime operand), so a graph captured for l_pad * depth tokens does no
+  // tensor work for padding beyond the next multiple of 16.
+  const int n_tiles = max(1, (n_live + BN - 1) / BN);
+  const int tw = min(BN, ((n_live + n_tiles - 1) / n_tiles + 15) / 16 * 16);
   const int num_kb = args.K / kBK;
   // Split-K factor: from device metadata when the plan is chosen per batch (pre-graph H2D).
   const int splits = args.splits_dev ? max(1, *args.splits_dev) : args.splits;
@@ -104,13 +110,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // MMA N of the tile starting at n0 (a multiple of 16, <= tw).
+  auto mma_n = [&](int n0) { return min(tw, (n_live - n0 + 15) / 16 * 16); };
   auto decode = [&](int w, int& s, int& m0, int& n0, int& kb0, int& kb1) {
     const int n = w % n_tiles;
     const int rest = w / n_tiles;
     const int m = rest % m_tiles;
     s = rest / m_tiles;
     m0 = m * kBM * kPair + static_cast<int>(rank) * kBM;  // this CTA's 128 weight rows
-    n0 = n * BN;
+    n0 = n * tw;
     const int base = num_kb / splits, rem = num_kb % splits;
     kb0 = s * base + min(s, rem);
     kb1 = kb0 + base + (s < rem ? 1 : 0);
@@ -128,10 +136,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto load = [&](int stage, int kb, int m0, int n0, bool a_part, bool b_part) {
         const uint32_t bar = bar0 + stage * 8;
         if constexpr (kPair == 2) {
+          // The pair's MMA takes N/2 token rows from each CTA: rank r holds
+          // tokens [n0 + r*N/2, n0 + (r+1)*N/2) at the top of its B stage.
           if (a_part) tma_load_2d_pair(sA + stage * C::kABytes, &tmA, bar, kb * kBK, m0, pol_w);
           if (b_part)
             tma_load_2d_pair(sB + stage * C::kBBytes, &tmB, bar, kb * kBK,
-                             n0 + static_cast<int>(rank) * C::kBRows, pol_x);
+                             n0 + static_cast<int>(rank) * (mma_n(n0) / 2), pol_x);
         } else {
           if (a_part) tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * kBK, m0, pol_w);
           if (b_part) tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * kBK, n0, pol_x);
@@ -176,7 +186,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ----------------------------------------------------------- MMA issuer (leader of a pair)
     if (leader) {
-      constexpr uint32_t idesc = idesc_bf16(kBM * kPair, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -188,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t idesc = idesc_bf16(kBM * kPair, mma_n(n0));
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -235,13 +245,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       float bias = 0.f;
       if (args.mode == kEpiBf16 && args.bias)
         bias = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(args.bias)[m]);
+      const int ncols = min(tw, n_live - n0);  // live tokens of this tile
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        if (n0 + c >= n_live) break;  // uniform across the epilogue group
+      for (int c = 0; c < ncols; c += 16) {  // uniform across the epilogue group
         float v[16];
         tmem_ld16(t_addr + c, v);
         const int nbase = n0 + c;
-        const int cnt = min(16, n_live - nbase);
+        const int cnt = min(16, ncols - c);
         if (args.mode == kEpiF32Partial) {
           // 32 lanes x consecutive m: one full 128-byte line per token.
           float* dst = args.ws + (static_cast<size_t>(s) * args.ws_stride + nbase) * args.M + m;

@@ -331,14 +331,32 @@ void qkv_post(const QkvCtx& c, cudaStream_t st) {
   if (half % 4 != 0 || half > kQkvMaxHalf)
     throw std::runtime_error("qkv_post: head_dim must be a multiple of 8 and <= 256");
   const int units = (c.nq + 2 * c.nkv) * (half / 4);
-  const bool deep = c.s_cap > 2 && units <= 1024;
-  const int per = deep ? 1 : 4;
-  const int threads = std::max(((units + per - 1) / per + 31) / 32 * 32, half);
-  if (threads > 1024) throw std::runtime_error("qkv_post: too many heads for one CTA per token");
-  if (deep)
-    launch_k(qkv_post_kernel<1, 8>, dim3(c.t_cap), dim3(threads), 0, st, c);
-  else
-    launch_k(qkv_post_kernel<4, 1>, dim3(c.t_cap), dim3(threads), 0, st, c);
+  // Deep split-K: all partials of a unit in flight (U=1, SU=8), or U=2, SU=4
+  // when one unit per thread would exceed the register file (e.g. 56 heads).
+  auto threads_for = [&](int per) { return std::max(((units + per - 1) / per + 31) / 32 * 32, half); };
+  auto max_threads = [](const void* k) {
+    cudaFuncAttributes a{};
+    return cudaFuncGetAttributes(&a, k) == cudaSuccess ? a.maxThreadsPerBlock : 0;
+  };
+  static const int cap18 = max_threads(reinterpret_cast<const void*>(qkv_post_kernel<1, 8>));
+  static const int cap24 = max_threads(reinterpret_cast<const void*>(qkv_post_kernel<2, 4>));
+  static const int cap41 = max_threads(reinterpret_cast<const void*>(qkv_post_kernel<4, 1>));
+  auto fits = [&](const void* k, int threads) {
+    const int cap = k == reinterpret_cast<const void*>(qkv_post_kernel<1, 8>)   ? cap18
+                    : k == reinterpret_cast<const void*>(qkv_post_kernel<2, 4>) ? cap24
+                                                                                 : cap41;
+    return threads <= cap;
+  };
+  const bool deep = c.s_cap > 2;
+  if (deep && fits(reinterpret_cast<const void*>(qkv_post_kernel<1, 8>), threads_for(1))) {
+    launch_k(qkv_post_kernel<1, 8>, dim3(c.t_cap), dim3(threads_for(1)), 0, st, c);
+  } else if (deep && fits(reinterpret_cast<const void*>(qkv_post_kernel<2, 4>), threads_for(2))) {
+    launch_k(qkv_post_kernel<2, 4>, dim3(c.t_cap), dim3(threads_for(2)), 0, st, c);
+  } else if (fits(reinterpret_cast<const void*>(qkv_post_kernel<4, 1>), threads_for(4))) {
+    launch_k(qkv_post_kernel<4, 1>, dim3(c.t_cap), dim3(threads_for(4)), 0, st, c);
+  } else {
+    throw std::runtime_error("qkv_post: too many heads for one CTA per token");
+  }
 }
 
 void gather_rows(const int* n_rows, int r_cap, const int* idx, const bf16* src, bf16* dst, int h,

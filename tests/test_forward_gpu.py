@@ -110,7 +110,7 @@ def test_7b_shaped_two_layers():
     from paper_2601_11589_b200.instance import QWEN25_7B
     cfg = QWEN25_7B.with_layers(2)
     inst = PrefillInstance(cfg, max_tokens=1024, max_members=16, kv_pages=64)
-    inst.capture_graphs(lengths=(128, 256), depths=(1, 2))
+    inst.capture_graphs(lengths=(128, 256), depths=(1, 2))  # + chunk graphs 64..512
     oracle = FO.OracleModel(FO.with_layers(FO.QWEN25_7B, 2))
     pages = PageOracle(64)
     M = Member
@@ -118,6 +118,10 @@ def test_7b_shaped_two_layers():
     _compare(inst, oracle, pages, 256, 2, KIND_GRAPH, [M(0, 0, 200, 0), M(1, 1, 77, 0)], tol=tol)
     _compare(inst, oracle, pages, 128, 1, KIND_GRAPH, [M(2, 0, 100, 200)], tol=tol)
     _compare(inst, oracle, pages, 600, 1, KIND_STANDARD, [M(3, 2, 600, 0)], tol=tol)
+    # long prompt as C_l = 512 chunks: one-member standard launches replay the
+    # per-64-token chunk graphs (tcgen05 attention), the tail sees history 512
+    _compare(inst, oracle, pages, 512, 1, KIND_STANDARD, [M(4, 3, 512, 0)], tol=tol)
+    _compare(inst, oracle, pages, 300, 1, KIND_STANDARD, [M(4, 3, 300, 512)], tol=tol)
     # layer >= 1 inherits the residual-stream noise floor: <= 4 bf16 ulps at |x| < 4
     _kv_check(inst, oracle, 0, [0, 1], max_abs=6.25e-2, mean_abs=5e-3)
     inst.close()

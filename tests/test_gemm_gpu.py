@@ -101,3 +101,20 @@ def test_gemm_pair(M, Ntok, K, bn, mode, splits):
 def test_gemm_pair_live_count():
     got, ref = run_gemm(1024, 512, 512, mode=3, bn=256, pair=2, n_live=300)
     _close(got, ref, n_live=300)
+
+
+@pytest.mark.parametrize("M,Ntok,K,bn,mode,splits,pair,n_live", [
+    (1024, 256, 512, 256, 3, 1, 2, 187),    # one tile, MMA N = 192
+    (1024, 512, 512, 256, 3, 1, 2, 385),    # two balanced tiles of 208
+    (1536, 1024, 256, 256, 2, 1, 2, 777),   # SiLU epilogue, 4 tiles of 208
+    (3584, 256, 3584, 256, 1, 3, 2, 130),   # split-K partials, N = 144
+    (1024, 64, 512, 64, 1, 2, 2, 17),       # pair, N = 32 (16 rows per CTA)
+    (1024, 128, 512, 128, 0, 1, 1, 33),     # single CTA, N = 48
+    (1024, 2048, 512, 256, 3, 1, 2, 2047),  # 8 tiles of 256, last one N = 256 with 255 live
+])
+def test_gemm_dynamic_tile_width(M, Ntok, K, bn, mode, splits, pair, n_live):
+    """Token tiles sized from the live count (balanced widths, MMA N rounded to 16)."""
+    got, ref = run_gemm(M, Ntok, K, splits=splits, mode=mode, bn=bn, pair=pair, n_live=n_live, bias=(mode == 0))
+    _close(got, ref, n_live=n_live)
+    if mode in (0, 3):
+        assert torch.all(got[n_live:] == 0)
