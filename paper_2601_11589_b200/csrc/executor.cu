@@ -538,7 +538,9 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   const int base = static_cast<int>(blks.size());
   // One wave for the tcgen05 kernel (one CTA per SM), two for the warp-MMA one.
   const int ctas = base * m_.n_kv_heads, target = (attn_rows == kAttnTcRows ? 1 : 2) * num_sms();
-  const int f = std::min(32, ctas < target ? (target + ctas - 1) / ctas : 1);  // combine: <= 32 splits
+  // Round DOWN: a split that pushes the grid past one wave of resident CTAs
+  // only adds a partial round trip and a combine pass.
+  const int f = std::min(32, std::max(1, target / std::max(ctas, 1)));  // combine: <= 32 splits
   int nw = 0, nc = 0, n_items = base;
   std::vector<Blk> full;
   for (const Blk& b : blks) {
