@@ -64,6 +64,40 @@ int choose_splits(int M, int bn, int pair, int n_live, int s_cap, int sms) {
   return best_s;
 }
 
+// Per-batch (token tiles, split-K) plan. Weight-streaming batches (< 256 live
+// tokens) keep ceil(n/bn) tiles and the wave-quantisation split choice. For
+// tensor-bound batches the unit count m_tiles * n_tiles * splits is chosen so
+// the last wave is nearly full: time ~ waves * (tile width + 16) * (K-blocks
+// per split + 2), +3% per extra split (fp32 partial round trip). Tile widths
+// are multiples of 16 (the MMA N is a runtime operand).
+TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms) {
+  TilePlan t;
+  const int base = std::max(1, (n_live + p.bn - 1) / p.bn);
+  t.n_tiles = base;
+  if (n_live < 256) {
+    t.splits = choose_splits(M, p.bn, p.pair, n_live, p.s_cap, sms);
+    return t;
+  }
+  const int workers = sms / p.pair, m_tiles = M / (128 * p.pair), nk = K / 64;
+  const int nt_hi = std::min(p.nt_cap, (n_live + 15) / 16);
+  double best = 1e30;
+  for (int nt = base; nt <= nt_hi; ++nt) {
+    const int tw = ((n_live + nt - 1) / nt + 15) / 16 * 16;
+    if (nt > base && (nt - 1) * tw >= n_live) continue;  // same widths as a smaller count
+    for (int s = 1; s <= p.s_cap; ++s) {
+      const long units = long(m_tiles) * nt * s;
+      const double waves = static_cast<double>((units + workers - 1) / workers);
+      const double cost = waves * (tw + 16) * (double(nk) / s + 2.0) * (1.0 + 0.03 * (s - 1));
+      if (cost < best * (1 - 1e-9)) {
+        best = cost;
+        t.n_tiles = nt;
+        t.splits = s;
+      }
+    }
+  }
+  return t;
+}
+
 namespace {
 
 // bn: smallest power-of-two tile >= tokens (<= 256). CTA pairs
@@ -75,6 +109,8 @@ GemmPlan plan_gemm(int M, int K, int t_cap, bool allow_split, int sms) {
   GemmPlan p;
   p.bn = pow2_bn(std::min(t_cap, 256));
   p.pair = (p.bn >= 128 && M % 256 == 0) ? 2 : 1;
+  const int base_nt = (t_cap + p.bn - 1) / p.bn;
+  p.nt_cap = t_cap >= 256 ? std::min(4 * base_nt, (t_cap + 15) / 16) : base_nt;
   if (!allow_split) return p;
   p.s_cap = split_cap(K, t_cap);
   p.splits = choose_splits(M, p.bn, p.pair, t_cap, p.s_cap, sms);
@@ -264,6 +300,14 @@ void Instance::alloc_arena() {
 // key-range splits of short batches over long histories.
 int Instance::combine_cap_for(int t_cap, int r_cap) const {
   const int G = m_.n_q_heads / m_.n_kv_heads;
+  // A row block is split only when the unsplit grid fills at most half of
+  // the split target (<= 2 resident CTAs per SM), i.e. blocks * nkv <= SMs:
+  // no more than SMs / nkv blocks can need a combine.
+  const int split_blocks = (num_sms() + m_.n_kv_heads - 1) / m_.n_kv_heads;
+  return std::min({c_max_, (t_cap * G + kAttnRows - 1) / kAttnRows + r_cap, split_blocks});
+}
+int Instance::block_cap_for(int t_cap, int r_cap) const {
+  const int G = m_.n_q_heads / m_.n_kv_heads;
   return std::min(c_max_, (t_cap * G + kAttnRows - 1) / kAttnRows + r_cap);
 }
 int Instance::work_cap_for(int t_cap, int r_cap) const {
@@ -271,7 +315,7 @@ int Instance::work_cap_for(int t_cap, int r_cap) const {
   // room is 2 * SMs / nkv items (early-exit CTAs beyond the live count still
   // occupy SM slots and would delay the next GEMM's PDL weight prefetch).
   const int extra = std::min(kAttnSplitExtra, (2 * num_sms() + m_.n_kv_heads - 1) / m_.n_kv_heads);
-  return std::min(w_max_, combine_cap_for(t_cap, r_cap) + extra);
+  return std::min(w_max_, block_cap_for(t_cap, r_cap) + extra);
 }
 
 SplitPlan Instance::plan_for(int t_cap, int r_cap) const {
@@ -298,6 +342,7 @@ void Instance::gemm(const CUtensorMap& tm_w, const GemmPlan& p, GemmArgs g, cons
                     cudaStream_t st) {
   // With a device-side split count the grid is sized for the largest one allowed.
   g.splits = g.splits_dev ? p.s_cap : p.splits;
+  g.n_tiles_cap = p.nt_cap;
   gemm_launch(tm_w, act_map(x, x_rows, g.K, gemm_b_box_rows(p.bn, p.pair)), g, p.bn, st, 0, p.pair);
 }
 
@@ -321,7 +366,7 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
     bf16* kv_layer = kv_pool_ + layer_stride_ * l;
     // QKV projection -> fp32 split partials.
     GemmArgs g;
-    g.M = qkv_out; g.N = t_cap; g.K = h; g.n_dev = n_tok;
+    g.M = qkv_out; g.N = t_cap; g.K = h; g.n_dev = n_tok; g.ntiles_dev = md_.scalars + 8;
     g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
     if (fuse_epilogues_ && p.qkv.splits == 1 && D == 128) {
       // Bias + RoPE + q / paged-KV writes straight from TMEM (no fp32 round trip).
@@ -344,7 +389,7 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
     attention_prefill(ac, tm_kv_, D, work_cap, combine_cap, st);
     // O projection + residual + RMSNorm.
     g = GemmArgs{};
-    g.M = h; g.N = t_cap; g.K = nq * D; g.n_dev = n_tok;
+    g.M = h; g.N = t_cap; g.K = nq * D; g.n_dev = n_tok; g.ntiles_dev = md_.scalars + 9;
     g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
     const bool o_fused = fuse_epilogues_ && p.o.splits == 1;
     if (o_fused) {  // residual add in the epilogue; the norm kernel then reads x_resid only
@@ -357,12 +402,12 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
     resid_rmsnorm(rc, ws_, 0, o_fused ? nullptr : md_.scalars + 5, t_cap, x_resid_, w.g_mlp, x_norm_, st);
     // gate/up with fused SiLU*up.
     g = GemmArgs{};
-    g.M = 2 * I; g.N = t_cap; g.K = h; g.n_dev = n_tok;
+    g.M = 2 * I; g.N = t_cap; g.K = h; g.n_dev = n_tok; g.ntiles_dev = md_.scalars + 10;
     g.mode = kEpiSiluMul; g.out = act_; g.ldo = I;
     gemm(w.tm_gu, p.gu, g, x_norm_, t_max_, st);
     // down + residual + next RMSNorm.
     g = GemmArgs{};
-    g.M = h; g.N = t_cap; g.K = I; g.n_dev = n_tok;
+    g.M = h; g.N = t_cap; g.K = I; g.n_dev = n_tok; g.ntiles_dev = md_.scalars + 11;
     g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
     const bool d_fused = fuse_epilogues_ && p.d.splits == 1;
     if (d_fused) {
@@ -516,6 +561,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
     }
   }
   const int work_cap = work_cap_for(t_cap, r_cap);
+  const int combine_cap = combine_cap_for(t_cap, r_cap);
 
   // Attention work list: one item per 64-row block of (token, q-head) rows;
   // when the blocks cannot fill the GPU, long key ranges are split
@@ -545,7 +591,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   std::vector<Blk> full;
   for (const Blk& b : blks) {
     const int s = std::min(f, b.need / kMinSplitTiles);
-    if (s >= 2 && nw + s <= kAttnSplitCap && n_items + s - 1 <= work_cap) {
+    if (s >= 2 && nw + s <= kAttnSplitCap && n_items + s - 1 <= work_cap && nc < combine_cap) {
       mh_.combine[nc++] = make_int4(b.r, b.row0, nw, s);
       for (int k = 0; k < s; ++k)
         mh_.work[nw++] = make_int4(b.r, b.row0, k * b.need / s, (k + 1) * b.need / s);
@@ -564,12 +610,21 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
     const SplitPlan sp = plan_for(t_cap, r_cap);
     const int h = m_.hidden, D = m_.head_dim, sms = num_sms();
     const int qkv_out = (m_.n_q_heads + 2 * m_.n_kv_heads) * D;
-    auto live_s = [&](const GemmPlan& gp, int M, bool fused) {
-      return fused ? 1 : choose_splits(M, gp.bn, gp.pair, t, gp.s_cap, sms);
+    auto live = [&](GemmPlan gp, int M, int K, bool fused) {
+      if (fused) gp.s_cap = 1;  // fused epilogues need the whole K in one unit
+      return choose_tiles(M, K, gp, t, sms);
     };
-    mh_.scalars[4] = live_s(sp.qkv, qkv_out, fuse_epilogues_ && sp.qkv.splits == 1 && D == 128);
-    mh_.scalars[5] = live_s(sp.o, h, fuse_epilogues_ && sp.o.splits == 1);
-    mh_.scalars[6] = live_s(sp.d, h, fuse_epilogues_ && sp.d.splits == 1);
+    const TilePlan tq = live(sp.qkv, qkv_out, h, fuse_epilogues_ && sp.qkv.splits == 1 && D == 128);
+    const TilePlan to = live(sp.o, h, m_.n_q_heads * D, fuse_epilogues_ && sp.o.splits == 1);
+    const TilePlan tg = live(sp.gu, 2 * m_.intermediate, h, true);
+    const TilePlan td = live(sp.d, h, m_.intermediate, fuse_epilogues_ && sp.d.splits == 1);
+    mh_.scalars[4] = tq.splits;
+    mh_.scalars[5] = to.splits;
+    mh_.scalars[6] = td.splits;
+    mh_.scalars[8] = tq.n_tiles;
+    mh_.scalars[9] = to.n_tiles;
+    mh_.scalars[10] = tg.n_tiles;
+    mh_.scalars[11] = td.n_tiles;
   }
 
   last_h2d_bytes_ = 0;
@@ -577,7 +632,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
     if (bytes) lp_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_), "meta h2d");
     last_h2d_bytes_ += bytes;
   };
-  h2d(md_.scalars, mh_.scalars, 32);
+  h2d(md_.scalars, mh_.scalars, 48);
   h2d(md_.tokens, mh_.tokens, size_t(t) * 4);
   h2d(md_.positions, mh_.positions, size_t(t) * 4);
   h2d(md_.slots, mh_.slots, size_t(t) * 4);
@@ -650,9 +705,14 @@ double Instance::time_gemm(int layer, int which, int t_cap, int n_live, int iter
   // Same per-batch split-K choice as a forward with n_live tokens.
   mh_.scalars[0] = n_live;
   mh_.scalars[1] = std::min(n_live, r_max_);
-  mh_.scalars[4] = choose_splits(g.M, p->bn, p->pair, n_live, p->s_cap, num_sms());
+  GemmPlan pl = *p;
+  if (g.mode != kEpiF32Partial) pl.s_cap = 1;
+  const TilePlan tp = choose_tiles(g.M, g.K, pl, n_live, num_sms());
+  mh_.scalars[4] = tp.splits;
+  mh_.scalars[8] = tp.n_tiles;
+  g.ntiles_dev = md_.scalars + 8;
   if (g.mode == kEpiF32Partial) g.splits_dev = md_.scalars + 4;
-  lp_check(cudaMemcpyAsync(md_.scalars, mh_.scalars, 32, cudaMemcpyHostToDevice, stream_), "meta");
+  lp_check(cudaMemcpyAsync(md_.scalars, mh_.scalars, 48, cudaMemcpyHostToDevice, stream_), "meta");
   lp_check(cudaStreamSynchronize(stream_), "sync");
   // Realistic operand values (unit-variance activations): an all-zero input
   // would under-state power draw and over-state the clock.

@@ -61,8 +61,13 @@ struct GemmPlan {
   int pair = 1;    // 2 = cta_group::2 CTA pair
   int splits = 1;  // split-K factor at full capacity (fp32 partial epilogues only)
   int s_cap = 1;   // largest split-K factor the workspace allows at this capacity
+  int nt_cap = 1;  // largest token-tile count a per-batch tile plan may pick
 };
 int choose_splits(int M, int bn, int pair, int n_live, int s_cap, int sms);
+struct TilePlan {
+  int n_tiles = 1, splits = 1;
+};
+TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms);
 struct SplitPlan {
   GemmPlan qkv, o, gu, d, lm;
 };
@@ -128,6 +133,7 @@ class Instance {
   CUtensorMap tm_kv_;
   int work_cap_for(int t_cap, int r_cap) const;
   int combine_cap_for(int t_cap, int r_cap) const;
+  int block_cap_for(int t_cap, int r_cap) const;
   float* x_resid_ = nullptr;
   bf16 *x_norm_ = nullptr, *q_ = nullptr, *attn_ = nullptr, *act_ = nullptr, *x_last_ = nullptr;
   float* ws_ = nullptr;

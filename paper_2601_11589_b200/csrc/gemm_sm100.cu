@@ -8,6 +8,7 @@
 //               so every activation byte crosses L2->SM once per 256 weight
 //               rows (not per 128) and per-SM shared-memory operand traffic
 //               halves. Used for token tiles of >= 128 columns.
+#include <algorithm>
 #include <cstdio>
 #include <mutex>
 #include <stdexcept>
@@ -78,7 +79,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // N = its live width rounded up to 16 (the instruction descriptor is a
   // runtime operand), so a graph captured for l_pad * depth tokens does no
   // tensor work for padding beyond the next multiple of 16.
-  const int n_tiles = max(1, (n_live + BN - 1) / BN);
+  int n_tiles = max(1, (n_live + BN - 1) / BN);
+  if (args.ntiles_dev) n_tiles = max(n_tiles, min(*args.ntiles_dev, (n_live + 15) / 16));
   const int tw = min(BN, ((n_live + n_tiles - 1) / n_tiles + 15) / 16 * 16);
   const int num_kb = args.K / kBK;
   // Split-K factor: from device metadata when the plan is chosen per batch (pre-graph H2D).
@@ -409,7 +411,7 @@ void launch_bn(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr_set = true;
   }
-  const int units = a.splits * (a.M / (kBM * kPair)) * ((a.N + BN - 1) / BN);
+  const int units = a.splits * (a.M / (kBM * kPair)) * std::max((a.N + BN - 1) / BN, a.n_tiles_cap);
   int grid = num_sms() / kPair;
   if (max_ctas > 0 && max_ctas / kPair < grid) grid = max_ctas / kPair;
   if (units < grid) grid = units;

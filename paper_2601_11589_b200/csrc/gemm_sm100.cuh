@@ -45,6 +45,10 @@ struct GemmArgs {
   int splits = 1;       // split-K factor
   const int* splits_dev = nullptr;  // optional device-side split-K factor (overrides `splits`)
   const int* n_dev = nullptr;  // optional device-side live token count (<= N)
+  // Optional device-side token-tile count (per-batch tile plan; clamped to
+  // [ceil(n_live / bn), ceil(n_live / 16)]); n_tiles_cap bounds it for the grid.
+  const int* ntiles_dev = nullptr;
+  int n_tiles_cap = 0;
   int mode = kEpiBf16;
   void* out = nullptr;
   int ldo = 0;

@@ -53,6 +53,7 @@ def main():
     ap.add_argument("--lengths", default="8,16,32,64,128,256")
     ap.add_argument("--depths", default="1,2,4,8,16,32,64")
     ap.add_argument("--long", action="store_true", help="also 512-token chunks at H in {0,512,1536,3584}")
+    ap.add_argument("--long-first", action="store_true", help="run the long chunks before the graph buckets")
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
@@ -112,12 +113,17 @@ def main():
               f"{r['hbm_gbs']:7.0f} GB/s ({r['frac_hbm']:.2f})  {r['tflops']:7.1f} TF/s "
               f"({r['frac_tensor_sustained']:.2f} sus)  roofline {r['frac_roofline']:.2f}", flush=True)
 
+    def longs():
+        for H in (0, 512, 1536, 3584):
+            run(512, 1, KIND_STANDARD, H, "long")
+
+    if a.long and a.long_first:
+        longs()
     for dp in depths:
         for lp in lengths:
             run(lp, dp, KIND_GRAPH, a.hist, "graph")
-    if a.long:
-        for H in (0, 512, 1536, 3584):
-            run(512, 1, KIND_STANDARD, H, "long")
+    if a.long and not a.long_first:
+        longs()
     out = {"model": a.model, "hist": a.hist, "peaks": {"hbm_gbs": hbm / 1e9, "tc_burst_tflops": tc_burst / 1e12,
                                                         "tc_sustained_tflops": tc_sus / 1e12}, "buckets": res}
     p = Path(a.out or f"gpurun_out/buckets_{a.model}_h{a.hist}.json")
