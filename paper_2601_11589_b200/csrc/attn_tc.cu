@@ -4,15 +4,22 @@
 //
 // One CTA = 128 packed (token, q-head) rows of one KV group x a key range.
 // Roles (192 threads):
-//   warp 0   TMA producer: K and V pages (2 pages = 128 keys per step) into a
-//            2-stage ring, laid out [d-half][128 keys][128 B] (128B swizzle);
+//   warp 0   TMA producers (lane 0 K, lane 1 V): pages (2 pages = 128 keys
+//            per step) into separate 2-stage K and V rings, laid out
+//            [d-half][128 keys][128 B] (128B swizzle);
 //   warp 1   MMA issuer (one thread):  S = Q K^T into TMEM (double-buffered,
 //            so S(j+1) overlaps the softmax of j), then O += P V with V as an
 //            MN-major operand (no transpose pass) and O resident in TMEM;
-//   warps 2-5 softmax: thread = query row = TMEM lane. tcgen05.ld of its S
-//            row, causal mask, online softmax in the log2 domain, P -> smem
-//            (bf16, 128B swizzle), O rescaled in TMEM only when the row max
-//            grew; epilogue O / l -> bf16 (or fp32 partial for key splits).
+//   warps 2-9 softmax, two warpgroups: query row = TMEM lane (warp % 4
+//            selects the lane quarter), group 0 owns key/d columns 0-63 and
+//            group 1 columns 64-127 of that row, so each thread does half a
+//            row per step. tcgen05.ld of its S half, causal mask, row max
+//            exchanged with the partner thread through smem (one named
+//            barrier per quarter per step), online softmax in the log2 domain
+//            with LAZY rescaling (the reference max moves only when a row max
+//            grows by > 2^8, so O in TMEM is rarely touched), P -> smem (bf16,
+//            128B swizzle); epilogue O / l -> bf16 (or fp32 partial for key
+//            splits).
 // Numerics match the mma.sync path (and the oracle's storage points): fp32
 // scores, bf16 P, fp32 O accumulation; key tiles of 128 instead of 64 change
 // only the online-softmax rescale points.
@@ -32,21 +39,34 @@ constexpr int kRows = 128;
 constexpr int kKeys = 128;                 // keys per step (2 pages)
 constexpr int kHalfBytes = kRows * 128;    // [128 rows][64 elems] bf16 = 16 KiB
 constexpr int kQBytes = 2 * kHalfBytes;    // Q / P / K / V tile: 32 KiB each
-constexpr int kStages = 2;
-constexpr int kThreads = 192;
+constexpr int kKStages = 3;  // K runs a step further ahead (S(s+2) is issued right after PV(s))
+constexpr int kVStages = 2;
+constexpr int kThreads = 320;
+constexpr int kSoftmaxWarps = 8;
+constexpr float kRescaleTau = 8.0f;  // log2 units: P <= 2^8 between rescales
 
 struct TcSmem {
   static constexpr int kQ = 0;
   static constexpr int kP = kQ + kQBytes;
   static constexpr int kK = kP + kQBytes;                 // [stage][32 KiB]
-  static constexpr int kV = kK + kStages * kQBytes;       // [stage][32 KiB]
-  static constexpr int kBars = kV + kStages * kQBytes;
-  static constexpr int kTotal = kBars + 256;
+  static constexpr int kV = kK + kKStages * kQBytes;      // [stage][32 KiB]
+  static constexpr int kBars = kV + kVStages * kQBytes;
+  static constexpr int kRed = kBars + 192;                // float [2 parity][2 group][128 rows]
+  static constexpr int kTotal = kRed + 2 * 2 * kRows * 4;  // 231,616 B of the 232,448 B limit
 };
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void st_shared_f32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ float ld_shared_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gmem) {
@@ -61,32 +81,43 @@ __device__ __forceinline__ uint32_t tile_addr(uint32_t base, int r, int c) {
 
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap kvm, const AttnCtx c) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // No alignment slack fits beside 3 K stages: the dynamic window must start
+  // 1024-byte aligned (128B-swizzle atoms); trap loudly if it ever does not.
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TcSmem::kBars);
-  uint64_t* kv_full = bars;        // [2]
-  uint64_t* kv_empty = bars + 2;   // [2]
+  // K and V have separate rings: K(s) is released as soon as S(s) retires,
+  // so the load of K(s+2) overlaps softmax(s) and PV(s); V(s) after PV(s).
+  uint64_t* k_full = bars + 18;    // [3]
+  uint64_t* k_empty = bars + 21;   // [3]
   uint64_t* s_full = bars + 4;     // [2]
   uint64_t* s_empty = bars + 6;    // [2]
   uint64_t* p_ready = bars + 8;
   uint64_t* o_done = bars + 9;
   uint64_t* q_ready = bars + 10;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* v_full = bars + 14;    // [2]
+  uint64_t* v_empty = bars + 16;   // [2]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   pdl_trigger();
   const int wi = blockIdx.x;
   const bool live = wi < *c.n_work;
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
+    for (int i = 0; i < kKStages; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
     }
-    mbar_init(p_ready, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], kSoftmaxWarps);
+    }
+    mbar_init(p_ready, kSoftmaxWarps);
     mbar_init(o_done, 1);
-    mbar_init(q_ready, 4);
+    mbar_init(q_ready, kSoftmaxWarps);
     fence_mbar_init();
   }
   if (warp == 1 && live) tmem_alloc<512>(tmem_slot);
@@ -119,25 +150,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sK = smem_u32(smem + TcSmem::kK), sV = smem_u32(smem + TcSmem::kV);
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (elect_one()) {
+    // ------------------------------------------------------------ TMA producers
+    // lane 0 streams K pages, lane 1 V pages (each into its own 2-stage ring).
+    if (lane < 2) {
+      const bool is_v = lane == 1;
+      uint64_t* full = is_v ? v_full : k_full;
+      uint64_t* empty = is_v ? v_empty : k_empty;
+      uint8_t* ring = smem + (is_v ? TcSmem::kV : TcSmem::kK);
+      const int ns = is_v ? kVStages : kKStages;
       for (int s = 0; s < n_steps; ++s) {
-        const int st = s & 1;
-        mbar_wait(&kv_empty[st], ((s >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[st], 2 * kQBytes);
+        const int st = s % ns;
+        mbar_wait(&empty[st], ((s / ns) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[st], kQBytes);
         const int t0 = t_begin + 2 * s;
         // A missing second page re-loads the first (finite values, masked).
         const int pg[2] = {pages[t0], t0 + 1 < t_end ? pages[t0 + 1] : pages[t0]};
 #pragma unroll
         for (int pi = 0; pi < 2; ++pi) {
-          const int plane_k = c.kv_plane0 + pg[pi] * 2 * c.nkv + g;
+          const int plane = c.kv_plane0 + pg[pi] * 2 * c.nkv + g + (is_v ? c.nkv : 0);
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            uint8_t* dk = smem + TcSmem::kK + st * kQBytes + hf * kHalfBytes + pi * 64 * 128;
-            uint8_t* dv = smem + TcSmem::kV + st * kQBytes + hf * kHalfBytes + pi * 64 * 128;
-            tma_load_3d(dk, &kvm, &kv_full[st], hf * 64, 0, plane_k);
-            tma_load_3d(dv, &kvm, &kv_full[st], hf * 64, 0, plane_k + c.nkv);
-          }
+          for (int hf = 0; hf < 2; ++hf)
+            tma_load_3d(ring + st * kQBytes + hf * kHalfBytes + pi * 64 * 128, &kvm, &full[st], hf * 64, 0, plane);
         }
       }
     }
@@ -150,17 +183,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     auto issue_s = [&](int s) {
       const int st = s & 1;
-      mbar_wait(&kv_full[st], (s >> 1) & 1);
+      const int kst = s % kKStages;
+      mbar_wait(&k_full[kst], (s / kKStages) & 1);
       if (s >= 2) mbar_wait(&s_empty[st], ((s >> 1) & 1) ^ 1);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k) {
           const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
-          tc_mma_bf16(tmem + st * kKeys, sdesc_sw128(sQ + off), sdesc_sw128(sK + st * kQBytes + off), idesc_s,
+          tc_mma_bf16(tmem + st * kKeys, sdesc_sw128(sQ + off), sdesc_sw128(sK + kst * kQBytes + off), idesc_s,
                       k > 0 ? 1u : 0u);
         }
         tc_commit(&s_full[st]);
+        tc_commit(&k_empty[kst]);
       }
       __syncwarp();
     };
@@ -169,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int st = s & 1;
       if (s + 1 < n_steps) issue_s(s + 1);
       mbar_wait(p_ready, s & 1);
+      mbar_wait(&v_full[st], (s >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -178,54 +214,72 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_mma_bf16(t_o, a, b, idesc_o, (s > 0 || k > 0) ? 1u : 0u);
         }
         tc_commit(o_done);
-        tc_commit(&kv_empty[st]);
+        tc_commit(&v_empty[st]);
       }
       __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
     const int q4 = warp & 3;
+    const int grp = (warp - 2) >> 2;           // 0: columns 0-63, 1: columns 64-127
     const int rt = q4 * 32 + lane;             // tile row == TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const int row = min(row0 + rt, rows_total - 1);
     const int j = row / G, hq = g * G + row % G;
     const int pos = H + j;
-    // Q row -> smem (swizzled), once.
+    const uint32_t red = smem_u32(smem + TcSmem::kRed);    // float [parity][grp][row]
+    const int bar_id = 1 + q4;                 // the two warps sharing this lane quarter
+    auto pair_sync = [&] { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
+    // This thread's half of the Q row -> smem (swizzled), once.
     const __nv_bfloat16* qrow = c.q + (qs + j) * ld_q + hq * kD;
 #pragma unroll
-    for (int ch = 0; ch < 16; ++ch) cp_async16(tile_addr(sQ, rt, ch), qrow + ch * 8);
+    for (int ch = 0; ch < 8; ++ch) cp_async16(tile_addr(sQ, rt, grp * 8 + ch), qrow + (grp * 8 + ch) * 8);
     asm volatile("cp.async.wait_all;" ::: "memory");
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(q_ready);
 
-    float m_run = -INFINITY, l_run = 0.f;
+    constexpr int kHalf = kKeys / 2;
+    float m_run = -INFINITY, l_run = 0.f;  // l_run: this thread's columns only
     for (int s = 0; s < n_steps; ++s) {
       const int st = s & 1;
       mbar_wait(&s_full[st], (s >> 1) & 1);
       tc_fence_after();
-      float sc[kKeys];
+      float sc[kHalf];
 #pragma unroll
-      for (int cc = 0; cc < kKeys / 16; ++cc) tmem_ld16(tmem + lane_off + st * kKeys + cc * 16, sc + cc * 16);
+      for (int cc = 0; cc < kHalf / 16; ++cc)
+        tmem_ld16(tmem + lane_off + st * kKeys + grp * kHalf + cc * 16, sc + cc * 16);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[st]);  // S buffer may be overwritten
 
-      const int kbase = (t_begin + 2 * s) * 64;
-      const int kvalid = min(kKeys, (t_end - t_begin - 2 * s) * 64);  // keys of real pages in this step
+      const int kbase = (t_begin + 2 * s) * 64 + grp * kHalf;
+      const int kvalid = min(kKeys, (t_end - t_begin - 2 * s) * 64) - grp * kHalf;  // keys of real pages
       float mx = -INFINITY;
+      if (kvalid >= kHalf && kbase + kHalf - 1 <= pos) {  // whole half visible: no mask (the bulk of long histories)
 #pragma unroll
-      for (int k = 0; k < kKeys; ++k) {
-        if (k >= kvalid || kbase + k > pos) sc[k] = -INFINITY;
-        mx = fmaxf(mx, sc[k]);
+        for (int k = 0; k < kHalf; ++k) mx = fmaxf(mx, sc[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < kHalf; ++k) {
+          if (k >= kvalid || kbase + k > pos) sc[k] = -INFINITY;
+          mx = fmaxf(mx, sc[k]);
+        }
       }
-      const float m_new = fmaxf(m_run, mx * c.scale_log2);
+      const uint32_t rb = red + (s & 1) * 2 * kRows * 4;
+      st_shared_f32(rb + (grp * kRows + rt) * 4, mx);
+      pair_sync();
+      mx = fmaxf(mx, ld_shared_f32(rb + ((grp ^ 1) * kRows + rt) * 4));
+      const float m_cand = fmaxf(m_run, mx * c.scale_log2);
+      // Lazy rescale: keep the reference max unless the row max outgrew it.
+      const bool grow = m_cand > m_run + kRescaleTau || (m_run == -INFINITY && m_cand != -INFINITY);
+      const float m_new = grow ? m_cand : m_run;
       const float m_use = m_new == -INFINITY ? 0.f : m_new;
-      const float corr = exp2f(m_run - m_use);
+      const float corr = grow ? exp2f(m_run - m_use) : 1.f;
       m_run = m_new;
       float sum = 0.f;
 #pragma unroll
-      for (int k = 0; k < kKeys; ++k) {
+      for (int k = 0; k < kHalf; ++k) {
         sc[k] = exp2f(sc[k] * c.scale_log2 - m_use);
         sum += sc[k];
       }
@@ -236,9 +290,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(o_done, (s - 1) & 1);
         tc_fence_after();
         if (__any_sync(0xffffffffu, corr != 1.f)) {
-          const uint32_t t_o = tmem + lane_off + 2 * kKeys;
+          const uint32_t t_o = tmem + lane_off + 2 * kKeys + grp * (kD / 2);
 #pragma unroll 1
-          for (int cc = 0; cc < kD / 16; ++cc) {
+          for (int cc = 0; cc < kD / 32; ++cc) {
             float o[16];
             tmem_ld16(t_o + cc * 16, o);
 #pragma unroll
@@ -248,16 +302,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_wait_st();
         }
       }
-      // P row (bf16) -> smem in the swizzled K-major layout of the A operand.
+      // P half-row (bf16) -> smem: keys 0-63 are swizzle half 0, 64-127 half 1.
 #pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {
+      for (int ch = 0; ch < 8; ++ch) {
         uint4 w;
         w.x = pack_bf16x2(sc[ch * 8 + 0], sc[ch * 8 + 1]);
         w.y = pack_bf16x2(sc[ch * 8 + 2], sc[ch * 8 + 3]);
         w.z = pack_bf16x2(sc[ch * 8 + 4], sc[ch * 8 + 5]);
         w.w = pack_bf16x2(sc[ch * 8 + 6], sc[ch * 8 + 7]);
-        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(tile_addr(sP, rt, ch)), "r"(w.x), "r"(w.y),
-                     "r"(w.z), "r"(w.w)
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(tile_addr(sP, rt, grp * 8 + ch)), "r"(w.x),
+                     "r"(w.y), "r"(w.z), "r"(w.w)
                      : "memory");
       }
       fence_proxy_async_smem();
@@ -266,17 +320,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(p_ready);
     }
 
-    // Epilogue: O row / l.
+    // Epilogue: O row / l, l = both groups' partial sums (same reference max).
+    // (the parity buffer of step n_steps was last read before step n_steps-1's barrier)
+    const uint32_t lsum = red + (n_steps & 1) * 2 * kRows * 4;
+    st_shared_f32(lsum + (grp * kRows + rt) * 4, l_run);
+    pair_sync();
+    const float l_tot = l_run + ld_shared_f32(lsum + ((grp ^ 1) * kRows + rt) * 4);
     if (n_steps > 0) {
       mbar_wait(o_done, (n_steps - 1) & 1);
       tc_fence_after();
     }
-    const uint32_t t_o = tmem + lane_off + 2 * kKeys;
+    const uint32_t t_o = tmem + lane_off + 2 * kKeys + grp * (kD / 2);
     if (!partial) {
-      const float inv = 1.f / l_run;
-      __nv_bfloat16* dst = c.out + (qs + j) * ld_q + hq * kD;
+      const float inv = 1.f / l_tot;
+      __nv_bfloat16* dst = c.out + (qs + j) * ld_q + hq * kD + grp * (kD / 2);
 #pragma unroll 1
-      for (int cc = 0; cc < kD / 16; ++cc) {
+      for (int cc = 0; cc < kD / 32; ++cc) {
         float o[16];
         tmem_ld16(t_o + cc * 16, o);
         if (row0 + rt < rows_total) {
@@ -290,17 +349,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else {
       const size_t slab = static_cast<size_t>(wi) * c.nkv + g;
-      float* dst = c.ws_o + (slab * kRows + rt) * kD;
+      float* dst = c.ws_o + (slab * kRows + rt) * kD + grp * (kD / 2);
 #pragma unroll 1
-      for (int cc = 0; cc < kD / 16; ++cc) {
+      for (int cc = 0; cc < kD / 32; ++cc) {
         float o[16];
         tmem_ld16(t_o + cc * 16, o);
 #pragma unroll
         for (int i = 0; i < 16; i += 4)
           *reinterpret_cast<float4*>(dst + cc * 16 + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
       }
-      c.ws_ml[(slab * kRows + rt) * 2 + 0] = m_run;
-      c.ws_ml[(slab * kRows + rt) * 2 + 1] = l_run;
+      if (grp == 0) {
+        c.ws_ml[(slab * kRows + rt) * 2 + 0] = m_run;
+        c.ws_ml[(slab * kRows + rt) * 2 + 1] = l_tot;
+      }
     }
   }
 
@@ -315,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 void attention_prefill_tc(const AttnCtx& c, const CUtensorMap& kv_map, int work_cap, cudaStream_t st) {
-  constexpr int smem = 1024 + TcSmem::kTotal;
+  constexpr int smem = TcSmem::kTotal;
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
