@@ -71,17 +71,18 @@ def load_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
 
 
-def committed_traffic(t_cap: int):
-    """DRAM bytes per launch of the dominant kernel from the committed
-    `ncu --set full` capture (profiles/r01_dominant_kernel.json), if it was
-    taken at this step capacity; else None."""
+def committed_traffic(t_cap: int, n_live: int):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed `ncu --set full` captures (profiles/r01_dominant_kernel.json),
+    if one was taken at this step capacity and live token count; else None."""
     p = ROOT / "profiles" / "r01_dominant_kernel.json"
     if not p.exists():
         return None
     d = json.loads(p.read_text())
-    if d.get("t_cap") != t_cap:
-        return None
-    return d.get("dram_bytes_per_launch")
+    for c in d.get("captures", []):
+        if c.get("t_cap") == t_cap and c.get("n_live") == n_live:
+            return c.get("dram_bytes_per_launch")
+    return None
 
 
 class ClockSampler:
@@ -449,7 +450,7 @@ def run_ours(args) -> None:
                                "gpu_req_per_s": st.completed / (st.gpu_ms_total / 1000.0)},
             "roofline": {"kernel": "gemm_bf16_tn_kernel gate/up (+SiLU*up)", "bound": "hbm" if hbm_bound else "tensor",
                          "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-                         "traffic": committed_traffic(t_cap), "t_cap": t_cap, "n_live": n_live, "avg_ms": gu_ms,
+                         "traffic": committed_traffic(t_cap, n_live), "t_cap": t_cap, "n_live": n_live, "avg_ms": gu_ms,
                          "peak_src": peaks["src"],
                          "forward_hbm_gbs": fw_bytes / (t_max * 1e-3) / 1e9 / (1 if ws == 1 else ws),
                          "forward_tflops": fw_flops / (t_max * 1e-3) / 1e12 / (1 if ws == 1 else ws)},
