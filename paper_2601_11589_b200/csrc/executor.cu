@@ -64,11 +64,16 @@ int choose_splits(int M, int bn, int pair, int n_live, int s_cap, int sms) {
   return best_s;
 }
 
+// Measured per-tile cost of a narrow token tile on B200 (7B projections at
+// T = 4096, forced tile counts): a tile of width tw costs ~ (tw + 55..105)
+// columns' worth of time (TMA issue, MMA issue, accumulator hand-off).
+constexpr double kTileOverheadCols = 80.0;
+
 // Per-batch (token tiles, split-K) plan. Weight-streaming batches (< 256 live
 // tokens) keep ceil(n/bn) tiles and the wave-quantisation split choice. For
 // tensor-bound batches the unit count m_tiles * n_tiles * splits is chosen so
-// the last wave is nearly full: time ~ waves * (tile width + 16) * (K-blocks
-// per split + 2), +3% per extra split (fp32 partial round trip). Tile widths
+// the last wave is nearly full: time ~ waves * (tile width + kTileOverheadCols)
+// * (K-blocks per split + 2), +3% per extra split (fp32 partial round trip). Tile widths
 // are multiples of 16 (the MMA N is a runtime operand).
 TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms) {
   TilePlan t;
@@ -87,7 +92,7 @@ TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms) {
     for (int s = 1; s <= p.s_cap; ++s) {
       const long units = long(m_tiles) * nt * s;
       const double waves = static_cast<double>((units + workers - 1) / workers);
-      const double cost = waves * (tw + 16) * (double(nk) / s + 2.0) * (1.0 + 0.03 * (s - 1));
+      const double cost = waves * (tw + kTileOverheadCols) * (double(nk) / s + 2.0) * (1.0 + 0.03 * (s - 1));
       if (cost < best * (1 - 1e-9)) {
         best = cost;
         t.n_tiles = nt;
