@@ -127,6 +127,25 @@ def test_7b_shaped_two_layers():
     inst.close()
 
 
+def test_32b_shaped_two_layers():
+    """Qwen2.5-32B shapes (h 5120, GQA group 5, 56 QKV heads -> the 2-unit
+    qkv_post schedule, 27648-wide MLP): a graph bucket, a re-prefill over the
+    cached pages and a 512-token chunk graph, 2 of the 64 layers."""
+    from paper_2601_11589_b200.instance import QWEN25_32B
+    cfg = QWEN25_32B.with_layers(2)
+    inst = PrefillInstance(cfg, max_tokens=1024, max_members=8, kv_pages=64)
+    inst.capture_graphs(lengths=(64, 256), depths=(1, 2))
+    oracle = FO.OracleModel(FO.with_layers(FO.QWEN25_32B, 2))
+    pages = PageOracle(64)
+    M = Member
+    tol = (5e-2, 1e-2, 0.9999)
+    _compare(inst, oracle, pages, 256, 2, KIND_GRAPH, [M(0, 0, 180, 0), M(1, 1, 33, 0)], tol=tol)
+    _compare(inst, oracle, pages, 64, 1, KIND_GRAPH, [M(2, 0, 40, 180)], tol=tol)
+    _compare(inst, oracle, pages, 512, 1, KIND_STANDARD, [M(3, 2, 512, 0)], tol=tol)
+    _kv_check(inst, oracle, 0, [0, 1], max_abs=6.25e-2, mean_abs=5e-3)
+    inst.close()
+
+
 def test_session_migration_between_instances():
     """Spatial disaggregation: a re-prefill lands on another instance; the
     session's KV pages move (lp_session_migrate; P2P over NVLink across
