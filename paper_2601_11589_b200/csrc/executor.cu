@@ -134,7 +134,12 @@ Instance::Instance(const lp_model_desc& m, const lp_instance_desc& d) : m_(m), d
   d_.page_size = kPage;
   if (d_.max_tokens <= 0) d_.max_tokens = 16384;
   if (d_.max_members <= 0) d_.max_members = 64;
-  if (const char* e = std::getenv("LP_FUSE_EPI"); e && e[0] == '1') fuse_epilogues_ = true;
+  if (const char* e = std::getenv("LP_FUSE_EPI")) {  // "1" both, "qkv", "resid"
+    const std::string v(e);
+    fuse_qkv_ = v == "1" || v == "qkv";
+    fuse_resid_ = v == "1" || v == "resid";
+  }
+  if (const char* e = std::getenv("LP_GRAPH_ATTN_TC_MIN")) graph_tc_min_ = std::atoi(e);
   if (const char* e = std::getenv("LP_ATTN_TC"); e && e[0] == '0') attn_tc_ = false;
   lp_check(cudaSetDevice(d.device), "cudaSetDevice");
   lp_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
@@ -352,7 +357,7 @@ void Instance::gemm(const CUtensorMap& tm_w, const GemmPlan& p, GemmArgs g, cons
 }
 
 void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph) {
-  const int attn_rows = graph ? kAttnRows : attn_rows_;
+  const int attn_rows = attn_rows_for(graph, t_cap);
   const int h = m_.hidden, I = m_.intermediate, D = m_.head_dim;
   const int nq = m_.n_q_heads, nkv = m_.n_kv_heads;
   const int qkv_out = (nq + 2 * nkv) * D;
@@ -373,7 +378,7 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
     GemmArgs g;
     g.M = qkv_out; g.N = t_cap; g.K = h; g.n_dev = n_tok; g.ntiles_dev = md_.scalars + 8;
     g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
-    if (fuse_epilogues_ && p.qkv.splits == 1 && D == 128) {
+    if (fuse_qkv_ && p.qkv.splits == 1 && D == 128) {
       // Bias + RoPE + q / paged-KV writes straight from TMEM (no fp32 round trip).
       g.mode = kEpiQkvRope;
       g.bias = w.bqkv;
@@ -396,7 +401,7 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
     g = GemmArgs{};
     g.M = h; g.N = t_cap; g.K = nq * D; g.n_dev = n_tok; g.ntiles_dev = md_.scalars + 9;
     g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
-    const bool o_fused = fuse_epilogues_ && p.o.splits == 1;
+    const bool o_fused = fuse_resid_ && p.o.splits == 1;
     if (o_fused) {  // residual add in the epilogue; the norm kernel then reads x_resid only
       g.mode = kEpiResidAdd;
       g.resid = x_resid_;
@@ -414,7 +419,7 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
     g = GemmArgs{};
     g.M = h; g.N = t_cap; g.K = I; g.n_dev = n_tok; g.ntiles_dev = md_.scalars + 11;
     g.mode = kEpiF32Partial; g.ws = ws_; g.ws_stride = t_cap;
-    const bool d_fused = fuse_epilogues_ && p.d.splits == 1;
+    const bool d_fused = fuse_resid_ && p.d.splits == 1;
     if (d_fused) {
       g.mode = kEpiResidAdd;
       g.resid = x_resid_;
@@ -555,7 +560,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
       exec = it->second;
       t_cap = static_cast<int>(shape.l_pad * shape.depth);
       r_cap = shape.depth;
-      attn_rows = kAttnRows;
+      attn_rows = attn_rows_for(true, t_cap);
     }
   } else if (d_.use_graphs && shape.kind == LP_KIND_STANDARD && n == 1) {
     auto it = chunk_graphs_.find((t + kChunkGraphStep - 1) / kChunkGraphStep * kChunkGraphStep);
@@ -619,10 +624,10 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
       if (fused) gp.s_cap = 1;  // fused epilogues need the whole K in one unit
       return choose_tiles(M, K, gp, t, sms);
     };
-    const TilePlan tq = live(sp.qkv, qkv_out, h, fuse_epilogues_ && sp.qkv.splits == 1 && D == 128);
-    const TilePlan to = live(sp.o, h, m_.n_q_heads * D, fuse_epilogues_ && sp.o.splits == 1);
+    const TilePlan tq = live(sp.qkv, qkv_out, h, fuse_qkv_ && sp.qkv.splits == 1 && D == 128);
+    const TilePlan to = live(sp.o, h, m_.n_q_heads * D, fuse_resid_ && sp.o.splits == 1);
     const TilePlan tg = live(sp.gu, 2 * m_.intermediate, h, true);
-    const TilePlan td = live(sp.d, h, m_.intermediate, fuse_epilogues_ && sp.d.splits == 1);
+    const TilePlan td = live(sp.d, h, m_.intermediate, fuse_resid_ && sp.d.splits == 1);
     mh_.scalars[4] = tq.splits;
     mh_.scalars[5] = to.splits;
     mh_.scalars[6] = td.splits;

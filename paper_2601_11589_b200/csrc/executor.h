@@ -151,7 +151,13 @@ class Instance {
   // whose capacity plan has no split-K. Measured neutral against the split
   // reduction kernels, and they pin the runtime split-K to 1, so they are
   // opt-in (LP_FUSE_EPI=1); the default chooses split-K per batch.
-  bool fuse_epilogues_ = false;
+  bool fuse_qkv_ = false, fuse_resid_ = false;
+  // Graph replays of at least this many tokens use the tcgen05 attention
+  // kernel (LP_GRAPH_ATTN_TC_MIN); smaller graphs the warp-MMA one.
+  int graph_tc_min_ = 1 << 30;
+  int attn_rows_for(bool graph, int t_cap) const {
+    return (graph && t_cap < graph_tc_min_) ? kAttnRows : attn_rows_;
+  }
   // head_dim 128 attention on the tcgen05/TMEM kernel (128-row work items);
   // LP_ATTN_TC=0 selects the warp-MMA kernel (64-row items) instead.
   bool attn_tc_ = true;
