@@ -146,6 +146,7 @@ Instance::Instance(const lp_model_desc& m, const lp_instance_desc& d) : m_(m), d
   lp_check(cudaEventCreate(&ev_start_), "event");
   lp_check(cudaEventCreate(&ev_end_), "event");
   lp_check(cudaEventCreateWithFlags(&ev_h2d_, cudaEventDisableTiming), "event");
+  lp_check(cudaEventCreateWithFlags(&ev_mig_, cudaEventDisableTiming), "event");
   alloc_weights();
   alloc_arena();
 }
@@ -160,6 +161,7 @@ Instance::~Instance() {
   cudaEventDestroy(ev_start_);
   cudaEventDestroy(ev_end_);
   cudaEventDestroy(ev_h2d_);
+  cudaEventDestroy(ev_mig_);
   for (cudaEvent_t e : timers_)
     if (e) cudaEventDestroy(e);
   cudaStreamDestroy(stream_);
@@ -818,18 +820,48 @@ void Instance::migrate(Instance& src, Instance& dst, int64_t sid) {
   Session& ds = dst.sessions_[sid];
   ds.pages = dst.alloc_pages(static_cast<int>(ss.pages.size()));
   ds.kv_len = ss.kv_len;
-  lp_check(cudaStreamSynchronize(src.stream_), "src sync");
-  const size_t bytes = src.page_elems_ * 2;
-  for (int l = 0; l < src.m_.layers; ++l) {
-    for (size_t k = 0; k < ss.pages.size(); ++k) {
-      const bf16* from = src.kv_pool_ + src.layer_stride_ * l + size_t(ss.pages[k]) * src.page_elems_;
-      bf16* to = dst.kv_pool_ + dst.layer_stride_ * l + size_t(ds.pages[k]) * dst.page_elems_;
-      if (src.d_.device == dst.d_.device)
-        lp_check(cudaMemcpyAsync(to, from, bytes, cudaMemcpyDeviceToDevice, dst.stream_), "kv copy");
-      else
-        lp_check(cudaMemcpyPeerAsync(to, dst.d_.device, from, src.d_.device, bytes, dst.stream_), "kv p2p");
+  const int n = static_cast<int>(ss.pages.size());
+  // The source's pending forwards wrote these pages: order the copy after them.
+  lp_check(cudaSetDevice(src.d_.device), "set device");
+  lp_check(cudaEventRecord(src.ev_mig_, src.stream_), "src event");
+  lp_check(cudaSetDevice(dst.d_.device), "set device");
+  lp_check(cudaStreamWaitEvent(dst.stream_, src.ev_mig_, 0), "wait src");
+  bool peer = src.d_.device == dst.d_.device;
+  if (!peer) {
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, dst.d_.device, src.d_.device);
+    if (can) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(src.d_.device, 0);  // from dst's context
+      if (e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled) peer = true;
+      cudaGetLastError();  // clear a benign already-enabled error
     }
   }
+  if (peer) {
+    // One kernel on the destination: reads the source pool directly (same
+    // HBM, or the peer's HBM over NVLink) and writes the new pages.
+    int* ids = nullptr;
+    lp_check(cudaMallocAsync(reinterpret_cast<void**>(&ids), size_t(2) * n * sizeof(int), dst.stream_), "ids");
+    std::vector<int> h(2 * n);
+    for (int k = 0; k < n; ++k) {
+      h[k] = ss.pages[k];
+      h[n + k] = ds.pages[k];
+    }
+    lp_check(cudaMemcpyAsync(ids, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, dst.stream_), "ids h2d");
+    kv_page_copy(src.kv_pool_, src.layer_stride_, dst.kv_pool_, dst.layer_stride_, src.page_elems_, ids, ids + n, n,
+                 src.m_.layers, dst.stream_);
+    lp_check(cudaGetLastError(), "kv copy");
+    lp_check(cudaFreeAsync(ids, dst.stream_), "ids free");
+  } else {
+    const size_t bytes = src.page_elems_ * 2;
+    for (int l = 0; l < src.m_.layers; ++l) {
+      for (int k = 0; k < n; ++k) {
+        const bf16* from = src.kv_pool_ + src.layer_stride_ * l + size_t(ss.pages[k]) * src.page_elems_;
+        bf16* to = dst.kv_pool_ + dst.layer_stride_ * l + size_t(ds.pages[k]) * dst.page_elems_;
+        lp_check(cudaMemcpyPeerAsync(to, dst.d_.device, from, src.d_.device, bytes, dst.stream_), "kv p2p");
+      }
+    }
+  }
+  // The source may reuse the pages only after the copy read them.
   lp_check(cudaStreamSynchronize(dst.stream_), "migrate sync");
   src.session_release(sid);
 }

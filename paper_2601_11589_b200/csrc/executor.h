@@ -109,6 +109,7 @@ class Instance {
   lp_instance_desc d_;
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr, ev_h2d_ = nullptr;
+  cudaEvent_t ev_mig_ = nullptr;  // end of this instance's queued work, for a session migration
 
   // model
   std::vector<LayerW> layers_;

@@ -310,6 +310,26 @@ void init_weights(bf16* dst, size_t n, uint64_t seed, uint64_t tensor_id, float 
   init_weights_kernel<<<4096, 256, 0, st>>>(dst, n, seed, tensor_id, scale, interleave_rows, cols);
 }
 
+__global__ void kv_page_copy_kernel(const uint4* __restrict__ src_pool, size_t src_layer_stride,
+                                    uint4* __restrict__ dst_pool, size_t dst_layer_stride, size_t page_vec,
+                                    const int* __restrict__ src_pages, const int* __restrict__ dst_pages) {
+  const int k = blockIdx.x, l = blockIdx.y;
+  const uint4* s = src_pool + l * src_layer_stride + static_cast<size_t>(src_pages[k]) * page_vec;
+  uint4* d = dst_pool + l * dst_layer_stride + static_cast<size_t>(dst_pages[k]) * page_vec;
+  for (size_t i = threadIdx.x; i < page_vec; i += blockDim.x) d[i] = s[i];
+}
+
+void kv_page_copy(const bf16* src_pool, size_t src_layer_stride, bf16* dst_pool, size_t dst_layer_stride,
+                  size_t page_elems, const int* src_pages, const int* dst_pages, int n_pages, int layers,
+                  cudaStream_t st) {
+  if (n_pages <= 0) return;
+  if (page_elems % 8 != 0 || src_layer_stride % 8 != 0 || dst_layer_stride % 8 != 0)
+    throw std::runtime_error("kv_page_copy: pages must be 16-byte multiples");
+  kv_page_copy_kernel<<<dim3(n_pages, layers), 512, 0, st>>>(
+      reinterpret_cast<const uint4*>(src_pool), src_layer_stride / 8, reinterpret_cast<uint4*>(dst_pool),
+      dst_layer_stride / 8, page_elems / 8, src_pages, dst_pages);
+}
+
 void fill_bf16(bf16* dst, size_t n, float v, cudaStream_t st) {
   fill_kernel<<<1024, 256, 0, st>>>(dst, n, v);
 }

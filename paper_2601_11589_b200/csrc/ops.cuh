@@ -19,6 +19,14 @@ void init_weights(bf16* dst, size_t n, uint64_t seed, uint64_t tensor_id, float 
                   int interleave_rows, int cols, cudaStream_t st);
 void fill_bf16(bf16* dst, size_t n, float v, cudaStream_t st);
 
+// Session-KV migration: copy `n_pages` pages of every layer from one paged
+// pool to another (page ids in device memory). `src_pool` may be a peer
+// device's pool (read over NVLink with peer access enabled). One launch moves
+// the whole session: grid (pages, layers), 16-byte vector copies.
+void kv_page_copy(const bf16* src_pool, size_t src_layer_stride, bf16* dst_pool, size_t dst_layer_stride,
+                  size_t page_elems, const int* src_pages, const int* dst_pages, int n_pages, int layers,
+                  cudaStream_t st);
+
 struct RowCtx {
   const int* n_live;  // device scalar: live tokens
   int t_cap;          // grid size (tokens) the launch was built for
