@@ -87,7 +87,30 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         if verbose:
             print(f"linked {LIB}", flush=True)
     stamp.write_text(digest)
+    build_examples(verbose)
     return LIB
+
+
+EXAMPLES = ROOT / "examples"
+
+
+def build_examples(verbose: bool = False) -> None:
+    """Plain-C consumers of the C ABI (examples/*.c) -> build/examples/, linked
+    against the in-tree liblaps_prefill.so (rpath to the package dir)."""
+    out = ROOT / "build" / "examples"
+    out.mkdir(parents=True, exist_ok=True)
+    for src in sorted(EXAMPLES.glob("*.c")):
+        exe = out / src.stem
+        if exe.exists() and exe.stat().st_mtime >= max(src.stat().st_mtime, LIB.stat().st_mtime):
+            continue
+        cmd = [os.environ.get("CC", "gcc"), "-std=c11", "-O2", "-Wall", "-Wextra", "-I", str(ROOT / "include"),
+               str(src), "-o", str(exe), "-L", str(PKG), "-llaps_prefill", "-Wl,-rpath," + str(PKG),
+               "-Wl,-rpath,$ORIGIN/../../paper_2601_11589_b200"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"example build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        if verbose:
+            print(f"built {exe}", flush=True)
 
 
 if __name__ == "__main__":
