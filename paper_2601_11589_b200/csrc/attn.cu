@@ -8,6 +8,7 @@
 #include <stdexcept>
 
 #include "attn.cuh"
+#include "attn_merge.cuh"
 #include "gemm_sm100.cuh"
 #include "launch.cuh"
 #include "ptx.cuh"
@@ -51,6 +52,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
   return base + (chunk >> 3) * (64 * 128) + row * 128 + (((chunk & 7) ^ (row & 7)) << 4);
 }
+
 
 template <int D>
 __global__ void __launch_bounds__(128)
@@ -262,12 +264,8 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// Merge the key-range splits of one (row block, kv head). Grid (groups, nkv,
-// block_rows / 8), one warp per row; lane s fetches split s's (m, l) (<= 32
-// splits), weights come from warp reductions, and the partial O rows are read
-// 8 splits at a time with all loads in flight (the merge is a chain of L2
-// round trips otherwise: it sits between attention and the O projection on
-// the short re-prefill path).
+
+// Merge grid: (row blocks that were split, nkv, block_rows / 8), one warp per row.
 template <int D>
 __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCtx c) {
   pdl_trigger();
@@ -275,55 +273,8 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCtx c) {
   const bool live = ci < *c.n_combine;
   pdl_wait();
   if (!live) return;
-  const int g = blockIdx.y;
-  const int G = c.nq / c.nkv;
   const int4 e = c.combine[ci];
-  const int r = e.x, row0 = e.y, first = e.z, ns = e.w;
-  const int rows_total = c.q_len[r] * G, qs = c.q_start[r];
-  const size_t ld_q = static_cast<size_t>(c.nq) * D;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int br = c.block_rows;
-  const int rl = blockIdx.z * 8 + warp;
-  const int row = row0 + rl;
-  if (rl >= br || row >= rows_total) return;
-  float m = -INFINITY, l = 0.f;
-  if (lane < ns) {
-    const size_t slab = static_cast<size_t>(first + lane) * c.nkv + g;
-    m = c.ws_ml[(slab * br + rl) * 2];
-    l = c.ws_ml[(slab * br + rl) * 2 + 1];
-  }
-  float m_star = m;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m_star = fmaxf(m_star, __shfl_xor_sync(0xffffffffu, m_star, o));
-  const float w_mine = (lane < ns && m != -INFINITY) ? exp2f(m - m_star) : 0.f;
-  float lsum = w_mine * l;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-  constexpr int kV = D / 32;
-  float acc[kV];
-#pragma unroll
-  for (int k = 0; k < kV; ++k) acc[k] = 0.f;
-  const size_t split_stride = static_cast<size_t>(c.nkv) * br * D;
-  const float* base = c.ws_o + ((static_cast<size_t>(first) * c.nkv + g) * br + rl) * D + lane;
-  for (int s0 = 0; s0 < ns; s0 += 8) {
-    float x[8][kV];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-#pragma unroll
-      for (int k = 0; k < kV; ++k) x[q][k] = s0 + q < ns ? base[(s0 + q) * split_stride + k * 32] : 0.f;
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float w = __shfl_sync(0xffffffffu, w_mine, (s0 + q) & 31);
-#pragma unroll
-      for (int k = 0; k < kV; ++k) acc[k] += w * x[q][k];
-    }
-  }
-  const int j = row / G, hq = g * G + row % G;
-  __nv_bfloat16* dst = c.out + (qs + j) * ld_q + hq * D;
-  const float inv = 1.f / lsum;
-#pragma unroll
-  for (int k = 0; k < kV; ++k) dst[k * 32 + lane] = __float2bfloat16_rn(acc[k] * inv);
+  merge_row<D>(c, e.z, e.w, blockIdx.y, e.x, e.y, blockIdx.z * 8 + threadIdx.x / 32, threadIdx.x % 32);
 }
 
 template <int D>
@@ -335,6 +286,9 @@ void launch(const AttnCtx& c, const CUtensorMap& kvm, int work_cap, int combine_
     set = true;
   }
   launch_k(attn_prefill_kernel<D>, dim3(work_cap, c.nkv), dim3(128), smem, st, kvm, c);
+  // Graph-bucket shapes split long histories into many short key ranges
+  // (up to 32 per 64-row block): a separate merge grid (one warp per row,
+  // many CTAs) beats a serial merge by the last split CTA.
   launch_k(attn_combine_kernel<D>, dim3(combine_cap, c.nkv, c.block_rows / 8), dim3(256), 0, st, c);
 }
 
@@ -351,7 +305,6 @@ void attention_prefill(const AttnCtx& c, const CUtensorMap& kv_map, int head_dim
                        int combine_cap, cudaStream_t st) {
   if (head_dim == 128 && c.block_rows == kAttnTcRows) {
     attention_prefill_tc(c, kv_map, work_cap, st);
-    launch_k(attn_combine_kernel<128>, dim3(combine_cap, c.nkv, c.block_rows / 8), dim3(256), 0, st, c);
   } else if (head_dim == 128) {
     launch<128>(c, kv_map, work_cap, combine_cap, st);
   } else if (head_dim == 64) {

@@ -43,6 +43,7 @@ struct AttnCtx {
   int nq, nkv;
   float scale_log2;  // log2(e) / sqrt(d)
   int block_rows;    // rows per work item: 64 (warp-MMA kernel) or 128 (tcgen05 kernel)
+  int* comb_cnt = nullptr;  // [combine capacity][nkv] split arrival tickets (zero between launches)
 };
 
 constexpr int kAttnRows = 64;    // rows per CTA

@@ -1,0 +1,102 @@
+// Split-KV merge: merge_row is shared by the graph-path combine grid
+// (attn.cu) and the tcgen05 kernel, whose last split CTA of a row block merges
+// the block itself (few, long splits: no separate combine launch between
+// attention and the O projection).
+#pragma once
+#include <cuda_bf16.h>
+
+#include "attn.cuh"
+
+namespace lp {
+
+// Merge the key-range splits of one row of a split (row block, kv head):
+// lane s fetches split s's (m, l) (<= 32 splits), weights come from warp
+// reductions, and the partial O rows are read 8 splits at a time with all
+// loads in flight.
+template <int D>
+__device__ __forceinline__ void merge_row(const AttnCtx& c, int first, int ns, int g, int r, int row0, int rl,
+                                          int lane) {
+  const int G = c.nq / c.nkv;
+  const int rows_total = c.q_len[r] * G, qs = c.q_start[r];
+  const int br = c.block_rows;
+  const int row = row0 + rl;
+  if (rl >= br || row >= rows_total) return;
+  float m = -INFINITY, l = 0.f;
+  if (lane < ns) {
+    const size_t slab = static_cast<size_t>(first + lane) * c.nkv + g;
+    m = __ldcg(c.ws_ml + (slab * br + rl) * 2);
+    l = __ldcg(c.ws_ml + (slab * br + rl) * 2 + 1);
+  }
+  float m_star = m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m_star = fmaxf(m_star, __shfl_xor_sync(0xffffffffu, m_star, o));
+  const float w_mine = (lane < ns && m != -INFINITY) ? exp2f(m - m_star) : 0.f;
+  float lsum = w_mine * l;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  constexpr int kV = D / 32;
+  float acc[kV];
+#pragma unroll
+  for (int k = 0; k < kV; ++k) acc[k] = 0.f;
+  const size_t split_stride = static_cast<size_t>(c.nkv) * br * D;
+  const float* base = c.ws_o + ((static_cast<size_t>(first) * c.nkv + g) * br + rl) * D + lane;
+  for (int s0 = 0; s0 < ns; s0 += 8) {
+    float x[8][kV];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+#pragma unroll
+      for (int k = 0; k < kV; ++k) x[q][k] = s0 + q < ns ? __ldcg(base + (s0 + q) * split_stride + k * 32) : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float w = __shfl_sync(0xffffffffu, w_mine, (s0 + q) & 31);
+#pragma unroll
+      for (int k = 0; k < kV; ++k) acc[k] += w * x[q][k];
+    }
+  }
+  const size_t ld_q = static_cast<size_t>(c.nq) * D;
+  const int j = row / G, hq = g * G + row % G;
+  __nv_bfloat16* dst = c.out + (qs + j) * ld_q + hq * D;
+  const float inv = 1.f / lsum;
+#pragma unroll
+  for (int k = 0; k < kV; ++k) dst[k * 32 + lane] = __float2bfloat16_rn(acc[k] * inv);
+}
+
+// Called by every thread of a CTA that wrote a split partial (work item wi,
+// kv head g) after its partial stores: the last split of the row block to
+// arrive (atomic ticket per (combine entry, kv head), reset by that CTA for
+// the next launch / graph replay) merges all splits' rows with its warps.
+template <int D>
+__device__ __forceinline__ void attn_merge_if_last(const AttnCtx& c, int wi, int g, int n_warps, int* scratch) {
+  int& s_ci = scratch[0];
+  int& s_last = scratch[1];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ci = 0;
+    const int nc = *c.n_combine;
+    for (int k = 0; k < nc; ++k) {
+      const int4 e = c.combine[k];
+      if (wi >= e.z && wi < e.z + e.w) {
+        ci = k;
+        break;
+      }
+    }
+    const int ns = c.combine[ci].w;
+    int* cnt = c.comb_cnt + static_cast<size_t>(ci) * c.nkv + g;
+    const int old = atomicAdd(cnt, 1);
+    const int last = old == ns - 1;
+    if (last) *cnt = 0;
+    s_ci = ci;
+    s_last = last;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int4 e = c.combine[s_ci];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int rl = warp; rl < c.block_rows; rl += n_warps) merge_row<D>(c, e.z, e.w, g, e.x, e.y, rl, lane);
+}
+
+
+}  // namespace lp

@@ -27,6 +27,7 @@
 #include <stdexcept>
 
 #include "attn.cuh"
+#include "attn_merge.cuh"
 #include "launch.cuh"
 #include "ptx.cuh"
 
@@ -371,6 +372,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+  // Key split: the last split of this row block to finish merges it (the
+  // exchange buffer is free once every softmax warp is past the barrier).
+  if (partial) attn_merge_if_last<128>(c, wi, g, kThreads / 32, reinterpret_cast<int*>(smem + TcSmem::kRed));
 }
 
 }  // namespace

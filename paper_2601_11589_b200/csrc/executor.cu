@@ -268,6 +268,8 @@ void Instance::alloc_arena() {
   attn_rows_ = (D == 128 && attn_tc_) ? kAttnTcRows : kAttnRows;
   attn_ws_o_ = dmalloc<float>(size_t(kAttnSplitCap) * m_.n_kv_heads * attn_rows_ * D, allocs_);
   attn_ws_ml_ = dmalloc<float>(size_t(kAttnSplitCap) * m_.n_kv_heads * attn_rows_ * 2, allocs_);
+  attn_comb_cnt_ = dmalloc<int>(size_t(c_max_) * m_.n_kv_heads, allocs_);
+  lp_check(cudaMemsetAsync(attn_comb_cnt_, 0, size_t(c_max_) * m_.n_kv_heads * sizeof(int), stream_), "tickets");
   max_pages_ = static_cast<int>(std::min<int64_t>(n_pages_, 4096));
 
   // Metadata block: device + pinned host mirror with identical layout.
@@ -397,7 +399,8 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
     AttnCtx ac{md_.scalars + 2, md_.work, md_.scalars + 3, md_.combine, md_.q_start, md_.q_len, md_.hist,
                md_.page_table, md_.page_off, q_, static_cast<int>(int64_t(l) * n_pages_ * 2 * nkv), attn_,
                attn_ws_o_, attn_ws_ml_, nq, nkv,
-               static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D))), attn_rows};
+               static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D))), attn_rows,
+               attn_comb_cnt_};
     attention_prefill(ac, tm_kv_, D, work_cap, combine_cap, st);
     // O projection + residual + RMSNorm.
     g = GemmArgs{};
@@ -598,7 +601,9 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   const int ctas = base * m_.n_kv_heads, target = (attn_rows == kAttnTcRows ? 1 : 2) * num_sms();
   // Round DOWN: a split that pushes the grid past one wave of resident CTAs
   // only adds a partial round trip and a combine pass.
-  const int f = std::min(32, std::max(1, target / std::max(ctas, 1)));  // combine: <= 32 splits
+  // <= 32 splits for the graph path's merge grid; <= 4 for the tcgen05 kernel,
+  // whose last split CTA merges the block itself.
+  const int f = std::min(attn_rows == kAttnTcRows ? 4 : 32, std::max(1, target / std::max(ctas, 1)));
   int nw = 0, nc = 0, n_items = base;
   std::vector<Blk> full;
   for (const Blk& b : blks) {

@@ -131,6 +131,7 @@ class Instance {
   int t_max_ = 0, r_max_ = 0, w_max_ = 0, c_max_ = 0;
   float* attn_ws_o_ = nullptr;
   float* attn_ws_ml_ = nullptr;
+  int* attn_comb_cnt_ = nullptr;  // split arrival tickets: the last split CTA merges its row block
   CUtensorMap tm_kv_;
   int work_cap_for(int t_cap, int r_cap) const;
   int combine_cap_for(int t_cap, int r_cap) const;
