@@ -278,7 +278,8 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCtx c) {
 }
 
 template <int D>
-void launch(const AttnCtx& c, const CUtensorMap& kvm, int work_cap, int combine_cap, cudaStream_t st) {
+void launch(const AttnCtx& c, const CUtensorMap& kvm, int work_cap, int combine_cap, bool with_combine,
+            cudaStream_t st) {
   constexpr int smem = 1024 + 5 * 64 * D * 2 + 64;
   static bool set = false;
   if (!set) {
@@ -289,7 +290,7 @@ void launch(const AttnCtx& c, const CUtensorMap& kvm, int work_cap, int combine_
   // Graph-bucket shapes split long histories into many short key ranges
   // (up to 32 per 64-row block): a separate merge grid (one warp per row,
   // many CTAs) beats a serial merge by the last split CTA.
-  launch_k(attn_combine_kernel<D>, dim3(combine_cap, c.nkv, c.block_rows / 8), dim3(256), 0, st, c);
+  if (with_combine) launch_k(attn_combine_kernel<D>, dim3(combine_cap, c.nkv, c.block_rows / 8), dim3(256), 0, st, c);
 }
 
 }  // namespace
@@ -302,13 +303,13 @@ CUtensorMap make_kv_tmap(const void* pool, int64_t planes, int head_dim) {
 }
 
 void attention_prefill(const AttnCtx& c, const CUtensorMap& kv_map, int head_dim, int work_cap,
-                       int combine_cap, cudaStream_t st) {
+                       int combine_cap, cudaStream_t st, bool with_combine) {
   if (head_dim == 128 && c.block_rows == kAttnTcRows) {
     attention_prefill_tc(c, kv_map, work_cap, st);
   } else if (head_dim == 128) {
-    launch<128>(c, kv_map, work_cap, combine_cap, st);
+    launch<128>(c, kv_map, work_cap, combine_cap, with_combine, st);
   } else if (head_dim == 64) {
-    launch<64>(c, kv_map, work_cap, combine_cap, st);
+    launch<64>(c, kv_map, work_cap, combine_cap, with_combine, st);
   } else {
     throw std::runtime_error("attention: head_dim must be 64 or 128");
   }

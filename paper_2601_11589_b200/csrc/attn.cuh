@@ -55,9 +55,10 @@ constexpr int kAttnTcRows = 128;     // rows per CTA of the tcgen05 kernel (head
 // plane = (layer * n_pages + page) * 2 * nkv + (is_v * nkv + kv_head).
 CUtensorMap make_kv_tmap(const void* pool, int64_t planes, int head_dim);
 
-// grid_x = work capacity, grid_y = nkv. head_dim in {64, 128}.
+// grid_x = work capacity, grid_y = nkv. head_dim in {64, 128}. with_combine = false
+// drops the graph path's merge grid (a launch with no key-range splits).
 void attention_prefill(const AttnCtx& c, const CUtensorMap& kv_map, int head_dim, int work_cap,
-                       int combine_cap, cudaStream_t st);
+                       int combine_cap, cudaStream_t st, bool with_combine = true);
 // tcgen05/TMEM kernel (head_dim 128, block_rows 128); see attn_tc.cu.
 void attention_prefill_tc(const AttnCtx& c, const CUtensorMap& kv_map, int work_cap, cudaStream_t st);
 

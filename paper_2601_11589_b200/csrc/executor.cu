@@ -155,6 +155,7 @@ Instance::~Instance() {
   cudaSetDevice(d_.device);
   cudaStreamSynchronize(stream_);
   for (auto& [k, g] : graphs_) cudaGraphExecDestroy(g);
+  for (auto& [k, g] : graphs_nc_) cudaGraphExecDestroy(g);
   for (auto& [k, g] : chunk_graphs_) cudaGraphExecDestroy(g);
   for (void* p : allocs_) cudaFree(p);
   if (meta_host_) cudaFreeHost(meta_host_);
@@ -360,7 +361,7 @@ void Instance::gemm(const CUtensorMap& tm_w, const GemmPlan& p, GemmArgs g, cons
   gemm_launch(tm_w, act_map(x, x_rows, g.K, gemm_b_box_rows(p.bn, p.pair)), g, p.bn, st, 0, p.pair);
 }
 
-void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph) {
+void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph, bool combine) {
   const int attn_rows = attn_rows_for(graph, t_cap);
   const int h = m_.hidden, I = m_.intermediate, D = m_.head_dim;
   const int nq = m_.n_q_heads, nkv = m_.n_kv_heads;
@@ -401,7 +402,7 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
                attn_ws_o_, attn_ws_ml_, nq, nkv,
                static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D))), attn_rows,
                attn_comb_cnt_};
-    attention_prefill(ac, tm_kv_, D, work_cap, combine_cap, st);
+    attention_prefill(ac, tm_kv_, D, work_cap, combine_cap, st, combine);
     // O projection + residual + RMSNorm.
     g = GemmArgs{};
     g.M = h; g.N = t_cap; g.K = nq * D; g.n_dev = n_tok; g.ntiles_dev = md_.scalars + 9;
@@ -480,6 +481,7 @@ void Instance::capture_graphs(const std::vector<int64_t>& lens, const std::vecto
       const int64_t key = graph_key(L, dep);
       if (graphs_.count(key)) continue;
       graphs_[key] = capture_one(static_cast<int>(t_cap), dep, true);
+      graphs_nc_[key] = capture_one(static_cast<int>(t_cap), dep, true, false);
     }
   }
   for (int t_cap = kChunkGraphStep; t_cap <= std::min(kChunkGraphMax, t_max_); t_cap += kChunkGraphStep)
@@ -487,11 +489,11 @@ void Instance::capture_graphs(const std::vector<int64_t>& lens, const std::vecto
   lp_check(cudaStreamSynchronize(stream_), "capture sync");
 }
 
-cudaGraphExec_t Instance::capture_one(int t_cap, int r_cap, bool graph_attn) {
-  enqueue_forward(t_cap, r_cap, stream_, graph_attn);  // warm-up (no live work)
+cudaGraphExec_t Instance::capture_one(int t_cap, int r_cap, bool graph_attn, bool combine) {
+  enqueue_forward(t_cap, r_cap, stream_, graph_attn, combine);  // warm-up (no live work)
   cudaGraph_t graph;
   lp_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
-  enqueue_forward(t_cap, r_cap, stream_, graph_attn);
+  enqueue_forward(t_cap, r_cap, stream_, graph_attn, combine);
   lp_check(cudaStreamEndCapture(stream_, &graph), "end capture");
   cudaGraphExec_t exec;
   lp_check(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
@@ -664,11 +666,15 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
 
   lp_check(cudaEventRecord(ev_h2d_, stream_), "event");
   lp_check(cudaEventRecord(ev_start_, stream_), "event");
+  if (exec && nc == 0 && shape.kind == LP_KIND_GRAPH) {
+    auto it = graphs_nc_.find(graph_key(shape.l_pad, shape.depth));
+    if (it != graphs_nc_.end()) exec = it->second;  // no split: skip the merge grid
+  }
   if (exec) {
     lp_check(cudaGraphLaunch(exec, stream_), "graph launch");
   } else {
     // Standard / packed / uncaptured: eager launch sized to the live batch.
-    enqueue_forward(t_cap, r_cap, stream_, false);
+    enqueue_forward(t_cap, r_cap, stream_, false, nc > 0);
   }
   lp_check(cudaGetLastError(), "forward launch");
   lp_check(cudaEventRecord(ev_end_, stream_), "event");

@@ -98,7 +98,7 @@ class Instance {
   void alloc_weights();
   void alloc_arena();
   SplitPlan plan_for(int t_cap, int r_cap) const;
-  void enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph);
+  void enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph, bool combine = true);
   const CUtensorMap& act_map(const bf16* buf, int rows, int cols, int box_rows);
   void gemm(const CUtensorMap& tm_w, const GemmPlan& p, GemmArgs g, const bf16* x, int x_rows, cudaStream_t st);
   std::vector<int32_t> alloc_pages(int n);
@@ -173,7 +173,10 @@ class Instance {
   // the host cannot issue as fast as the GPU retires them.
   static constexpr int kChunkGraphStep = 64, kChunkGraphMax = 512;
   std::map<int, cudaGraphExec_t> chunk_graphs_;
-  cudaGraphExec_t capture_one(int t_cap, int r_cap, bool graph_attn);
+  cudaGraphExec_t capture_one(int t_cap, int r_cap, bool graph_attn, bool combine = true);
+  // Grid shapes also get a variant without the attention merge grid, replayed
+  // when no row block of the batch was split (every H = 0 batch, e.g.).
+  std::map<int64_t, cudaGraphExec_t> graphs_nc_;
   bool submitted_ = false;
  public:
   size_t last_h2d_bytes_ = 0, last_d2h_bytes_ = 0;  // host<->device bytes of the last submit / read
