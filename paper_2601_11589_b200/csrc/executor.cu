@@ -371,7 +371,8 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
   const int* n_mem = md_.scalars + 1;
   const RowCtx rc{n_tok, t_cap, h, m_.rms_eps};
   const int G = nq / nkv;
-  const int work_cap = work_cap_for(t_cap, r_cap);
+  // Without the merge grid no item is split: the grid needs no split room.
+  const int work_cap = combine ? work_cap_for(t_cap, r_cap) : block_cap_for(t_cap, r_cap);
   const int combine_cap = combine_cap_for(t_cap, r_cap);
   (void)G;
 
