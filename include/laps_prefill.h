@@ -128,6 +128,9 @@ int lp_read_logits(lp_instance* inst, float* out, size_t cap_floats);
 /* Host->device bytes copied by the last lp_submit (token ids + metadata)
  * and device->host bytes of the last lp_read_next_tokens. */
 int lp_last_io(lp_instance* inst, int64_t* h2d_bytes, int64_t* d2h_bytes);
+/* Kernels the last lp_submit put on the GPU (graph kernel nodes or eager
+ * launches): 1 + layers x (8 or 9) + 3. */
+int lp_last_launches(lp_instance* inst, int32_t* kernels);
 /* Device-side timing on the instance stream (CUDA events): record `slot`
  * (0..7); elapsed ms between two recorded slots (blocks on slot_b). */
 int lp_timer_record(lp_instance* inst, int32_t slot);

@@ -75,7 +75,7 @@ PUBLIC_SYMBOLS = [
     "lp_instance_create", "lp_instance_destroy", "lp_capture_graphs", "lp_submit", "lp_wait",
     "lp_read_next_tokens", "lp_read_logits", "lp_session_pages", "lp_session_release",
     "lp_read_kv", "lp_session_migrate", "lp_synth_token", "lp_last_error", "lp_version",
-    "lp_instance_model", "lp_timer_record", "lp_timer_elapsed", "lp_last_io",
+    "lp_instance_model", "lp_timer_record", "lp_timer_elapsed", "lp_last_io", "lp_last_launches",
 ]
 ENGINE_SYMBOLS = ["lp_sim_run", "lp_sim_trace"]  # include/laps_engine.h
 
@@ -107,6 +107,7 @@ def _declare(L: ctypes.CDLL) -> None:
     sig("lp_instance_model", c_i32, vp, ctypes.POINTER(ModelDesc))
     sig("lp_timer_record", c_i32, vp, c_i32)
     sig("lp_last_io", c_i32, vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64))
+    sig("lp_last_launches", c_i32, vp, ctypes.POINTER(c_i32))
     sig("lp_timer_elapsed", c_i32, vp, c_i32, c_i32, ctypes.POINTER(c_f64))
     sig("lpk_time_gemm", c_i32, vp, c_i32, c_i32, c_i32, c_i32, c_i32, ctypes.POINTER(c_f64))
     # kernel-level test hooks (include/laps_prefill_testing.h)

@@ -671,6 +671,13 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
     auto it = graphs_nc_.find(graph_key(shape.l_pad, shape.depth));
     if (it != graphs_nc_.end()) exec = it->second;  // no split: skip the merge grid
   }
+  {
+    // Kernel count of this forward (the enqueue_forward sequence).
+    const bool warp_attn = attn_rows != kAttnTcRows;
+    const bool merge_grid = warp_attn && nc > 0;  // the no-merge graph variant is used when nc == 0
+    const bool qkv_fused = fuse_qkv_ && plan_for(t_cap, r_cap).qkv.splits == 1 && m_.head_dim == 128;
+    last_launches_ = 1 + m_.layers * (7 + (qkv_fused ? 0 : 1) + (merge_grid ? 1 : 0)) + 3;
+  }
   if (exec) {
     lp_check(cudaGraphLaunch(exec, stream_), "graph launch");
   } else {
@@ -940,6 +947,12 @@ int lp_last_io(lp_instance* inst, int64_t* h2d_bytes, int64_t* d2h_bytes) {
   return lp::lp_guard([&] {
     if (h2d_bytes) *h2d_bytes = static_cast<int64_t>(inst->impl->last_h2d_bytes_);
     if (d2h_bytes) *d2h_bytes = static_cast<int64_t>(inst->impl->last_d2h_bytes_);
+  });
+}
+
+int lp_last_launches(lp_instance* inst, int32_t* kernels) {
+  return lp::lp_guard([&] {
+    if (kernels) *kernels = inst->impl->last_launches_;
   });
 }
 

@@ -180,6 +180,7 @@ class Instance {
   bool submitted_ = false;
  public:
   size_t last_h2d_bytes_ = 0, last_d2h_bytes_ = 0;  // host<->device bytes of the last submit / read
+  int last_launches_ = 0;                             // kernels of the last submit
  private:
   int last_n_members_ = 0;
 };

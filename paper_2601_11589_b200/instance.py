@@ -184,6 +184,12 @@ class PrefillInstance:
         _check(N.lib().lp_last_io(self._h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
 
+    def last_launches(self) -> int:
+        """Kernels the last submit put on the GPU (graph nodes or eager launches)."""
+        n = ctypes.c_int32()
+        _check(N.lib().lp_last_launches(self._h, ctypes.byref(n)))
+        return n.value
+
     def timer_record(self, slot: int) -> None:
         _check(N.lib().lp_timer_record(self._h, slot))
 

@@ -202,7 +202,10 @@ def test_long_history_split_kv():
     pages = PageOracle(256)
     _compare(inst, oracle, pages, 0, 0, KIND_PACKED, [Member(0, 1, 2000, 0)])
     _compare(inst, oracle, pages, 32, 2, KIND_GRAPH, [Member(1, 1, 20, 2000), Member(2, 2, 30, 0)])
+    assert inst.last_launches() == 1 + 2 * 9 + 3  # split history: the merge grid runs
     _kv_check(inst, oracle, 1, [0, 1])
+    _compare(inst, oracle, pages, 32, 2, KIND_GRAPH, [Member(3, 3, 20, 0)])
+    assert inst.last_launches() == 1 + 2 * 8 + 3  # no split: the merge-free graph variant
     inst.close()
     # 7B-shaped, 2 layers: 1500-token history + a 64-token chunk (eager -> tcgen05 kernel)
     from paper_2601_11589_b200.instance import QWEN25_7B
