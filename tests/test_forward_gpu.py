@@ -217,3 +217,25 @@ def test_long_history_split_kv():
     _compare(inst, oracle, pages, 0, 0, KIND_PACKED, [Member(0, 5, 1500, 0)], tol=tol)
     _compare(inst, oracle, pages, 0, 0, KIND_PACKED, [Member(1, 5, 64, 1500), Member(2, 6, 16, 0)], tol=tol)
     inst.close()
+
+
+def test_error_codes_mirror_reference_exceptions():
+    """LP_ERR_* statuses (laps_prefill.h): ShapeMismatch / ConfigError mirror
+    the reference's exceptions (cost_model.hpp:17-19, 78-80); pool exhaustion
+    is LP_ERR_OOM and leaves the instance usable; a re-prefill whose history
+    is not resident is refused."""
+    from paper_2601_11589_b200 import _native as N
+    from paper_2601_11589_b200.instance import ConfigError, ModelConfig
+    with pytest.raises(ConfigError):
+        PrefillInstance(ModelConfig(hidden=200, intermediate=704, layers=1, n_q_heads=4, n_kv_heads=2,
+                                    head_dim=64, vocab=1024), kv_pages=8)
+    inst = PrefillInstance(TINY, max_tokens=1024, max_members=8, kv_pages=4)  # 256 token slots
+    with pytest.raises(N.NativeError) as e:
+        inst.forward(0, 0, KIND_PACKED, [Member(0, 0, 300, 0)], np.zeros(300, np.int32))
+    assert "[-3]" in str(e.value)
+    inst.forward(0, 0, KIND_PACKED, [Member(1, 1, 100, 0)], np.zeros(100, np.int32))  # still usable
+    with pytest.raises(N.NativeError):
+        inst.forward(0, 0, KIND_PACKED, [Member(2, 2, 10, 50)], np.zeros(10, np.int32))  # history not resident
+    with pytest.raises(ShapeMismatch):
+        inst.forward(0, 0, KIND_PACKED, [], np.zeros(0, np.int32))
+    inst.close()
