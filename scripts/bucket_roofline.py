@@ -54,6 +54,7 @@ def main():
     ap.add_argument("--depths", default="1,2,4,8,16,32,64")
     ap.add_argument("--long", action="store_true", help="also 512-token chunks at H in {0,512,1536,3584}")
     ap.add_argument("--long-first", action="store_true", help="run the long chunks before the graph buckets")
+    ap.add_argument("--long-h", default="0,512,1536,3584", help="histories of the long chunks")
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
@@ -114,7 +115,7 @@ def main():
               f"({r['frac_tensor_sustained']:.2f} sus)  roofline {r['frac_roofline']:.2f}", flush=True)
 
     def longs():
-        for H in (0, 512, 1536, 3584):
+        for H in [int(x) for x in a.long_h.split(",")]:
             run(512, 1, KIND_STANDARD, H, "long")
 
     if a.long and a.long_first:

@@ -229,11 +229,14 @@ def test_error_codes_mirror_reference_exceptions():
     with pytest.raises(ConfigError):
         PrefillInstance(ModelConfig(hidden=200, intermediate=704, layers=1, n_q_heads=4, n_kv_heads=2,
                                     head_dim=64, vocab=1024), kv_pages=8)
-    inst = PrefillInstance(TINY, max_tokens=1024, max_members=8, kv_pages=4)  # 256 token slots
+    inst = PrefillInstance(TINY, max_tokens=1024, max_members=8, kv_pages=8)  # 512 token slots
+    inst.forward(0, 0, KIND_PACKED, [Member(0, 0, 300, 0)], np.zeros(300, np.int32))  # 5 pages
     with pytest.raises(N.NativeError) as e:
-        inst.forward(0, 0, KIND_PACKED, [Member(0, 0, 300, 0)], np.zeros(300, np.int32))
+        inst.forward(0, 0, KIND_PACKED, [Member(1, 1, 300, 0)], np.zeros(300, np.int32))  # 5 more: 3 free
     assert "[-3]" in str(e.value)
-    inst.forward(0, 0, KIND_PACKED, [Member(1, 1, 100, 0)], np.zeros(100, np.int32))  # still usable
+    inst.release(0)
+    inst.release(1)
+    inst.forward(0, 0, KIND_PACKED, [Member(1, 1, 300, 0)], np.zeros(300, np.int32))  # usable again
     with pytest.raises(N.NativeError):
         inst.forward(0, 0, KIND_PACKED, [Member(2, 2, 10, 50)], np.zeros(10, np.int32))  # history not resident
     with pytest.raises(ShapeMismatch):
