@@ -12,8 +12,11 @@
 // group ("GQA packing", 64 rows per CTA) so every page a CTA loads is reused
 // by all G query heads that share it. A work item is (member, row block, key
 // tile range): short batches over long histories are split along the key
-// range (flash-decoding style) and merged by a combine kernel, so the grid
-// fills the GPU even when few rows exist. Items are ordered heaviest first.
+// range (flash-decoding style) and merged afterwards — by a merge grid on
+// the graph path (attn.cu; graph variants without it replay batches that did
+// not split), by the last split CTA of the block in the tcgen05 kernel — so
+// the grid fills the GPU even when few rows exist. Items are ordered heaviest
+// first.
 // The grid is sized from capacity, never from H, so it lives inside the
 // per-shape CUDA graphs; the live work list comes from device memory.
 #pragma once
