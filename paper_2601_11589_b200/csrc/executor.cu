@@ -156,6 +156,7 @@ Instance::~Instance() {
   cudaStreamSynchronize(stream_);
   for (auto& [k, g] : graphs_) cudaGraphExecDestroy(g);
   for (auto& [k, g] : graphs_nc_) cudaGraphExecDestroy(g);
+  for (auto& [k, g] : graphs_tc_) cudaGraphExecDestroy(g);
   for (auto& [k, g] : chunk_graphs_) cudaGraphExecDestroy(g);
   for (void* p : allocs_) cudaFree(p);
   if (meta_host_) cudaFreeHost(meta_host_);
@@ -483,6 +484,7 @@ void Instance::capture_graphs(const std::vector<int64_t>& lens, const std::vecto
       if (graphs_.count(key)) continue;
       graphs_[key] = capture_one(static_cast<int>(t_cap), dep, true);
       graphs_nc_[key] = capture_one(static_cast<int>(t_cap), dep, true, false);
+      if (m_.head_dim == 128 && attn_tc_) graphs_tc_[key] = capture_one(static_cast<int>(t_cap), dep, false, true);
     }
   }
   for (int t_cap = kChunkGraphStep; t_cap <= std::min(kChunkGraphMax, t_max_); t_cap += kChunkGraphStep)
@@ -559,6 +561,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   // Grid-shape graph (warp-MMA attention), chunk graph for a one-member
   // standard launch (tcgen05 attention), else eager sized to the live batch.
   cudaGraphExec_t exec = nullptr;
+  bool tc_graph = false;
   int t_cap = std::min(std::max(16, (t + 15) / 16 * 16), t_max_);
   int r_cap = n;
   int attn_rows = attn_rows_;  // matches enqueue_forward
@@ -569,6 +572,14 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
       t_cap = static_cast<int>(shape.l_pad * shape.depth);
       r_cap = shape.depth;
       attn_rows = attn_rows_for(true, t_cap);
+      int64_t pairs = 0;
+      for (int i = 0; i < n; ++i) pairs += mem[i].new_tokens * (mem[i].history + mem[i].new_tokens);
+      auto jt = graphs_tc_.find(graph_key(shape.l_pad, shape.depth));
+      if (attn_rows != kAttnTcRows && pairs >= kGraphTcPairs && jt != graphs_tc_.end()) {
+        exec = jt->second;
+        attn_rows = kAttnTcRows;
+        tc_graph = true;
+      }
     }
   } else if (d_.use_graphs && shape.kind == LP_KIND_STANDARD && n == 1) {
     auto it = chunk_graphs_.find((t + kChunkGraphStep - 1) / kChunkGraphStep * kChunkGraphStep);
@@ -667,7 +678,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
 
   lp_check(cudaEventRecord(ev_h2d_, stream_), "event");
   lp_check(cudaEventRecord(ev_start_, stream_), "event");
-  if (exec && nc == 0 && shape.kind == LP_KIND_GRAPH) {
+  if (exec && nc == 0 && shape.kind == LP_KIND_GRAPH && !tc_graph) {
     auto it = graphs_nc_.find(graph_key(shape.l_pad, shape.depth));
     if (it != graphs_nc_.end()) exec = it->second;  // no split: skip the merge grid
   }

@@ -242,3 +242,24 @@ def test_error_codes_mirror_reference_exceptions():
     with pytest.raises(ShapeMismatch):
         inst.forward(0, 0, KIND_PACKED, [], np.zeros(0, np.int32))
     inst.close()
+
+
+def test_deep_reprefill_graph_uses_tcgen05_variant():
+    """A graph bucket whose attention work sum L (H + L) reaches the
+    threshold replays the tcgen05-attention graph variant (128-row blocks,
+    in-kernel split merge): results match the oracle like the warp-MMA
+    variant's."""
+    from paper_2601_11589_b200.instance import QWEN25_7B
+    cfg = QWEN25_7B.with_layers(2)
+    inst = PrefillInstance(cfg, max_tokens=2560, max_members=8, kv_pages=64)
+    inst.capture_graphs(lengths=(256,), depths=(2,))
+    oracle = FO.OracleModel(FO.with_layers(FO.QWEN25_7B, 2))
+    pages = PageOracle(64)
+    M = Member
+    tol = (5e-2, 1e-2, 0.9999)
+    _compare(inst, oracle, pages, 0, 0, KIND_PACKED, [M(0, 0, 1200, 0), M(1, 1, 1100, 0)], tol=tol)
+    # 2 x 200 x (1200 + 200) + ... >= 500K pairs -> tcgen05 variant (8 kernels per layer, merge in-kernel)
+    _compare(inst, oracle, pages, 256, 2, KIND_GRAPH, [M(2, 0, 200, 1200), M(3, 1, 190, 1100)], tol=tol)
+    assert inst.last_launches() == 1 + 2 * 8 + 3
+    _kv_check(inst, oracle, 0, [0, 1], max_abs=6.25e-2, mean_abs=5e-3)
+    inst.close()
