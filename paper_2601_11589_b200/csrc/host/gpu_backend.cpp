@@ -74,18 +74,23 @@ class GpuBackend final : public ForwardBackend {
     }
     stats_.gpu_forwards += 1;
     stats_.gpu_ms_total += ms;
-    Tokens t = 0;
-    for (const auto& row : call.rows) t += row.new_tokens;
+    Tokens t = 0, hist = 0;
+    double pairs = 0;  // attention (query, key) pairs: sum L (H + (L + 1) / 2)
+    for (const auto& row : call.rows) {
+      t += row.new_tokens;
+      hist += row.history;
+      pairs += static_cast<double>(row.new_tokens) * (static_cast<double>(row.history) + (row.new_tokens + 1) / 2.0);
+    }
     stats_.real_tokens += t;
     log_ << call.inst << ',' << static_cast<int>(call.kind) << ',' << call.shape.l_pad << ','
          << call.shape.depth << ',' << (call.shape.kind == ShapeKind::kGraph ? 1 : 0) << ',' << call.rows.size()
-         << ',' << t << ',' << call.model_service_ms << ',' << ms << '\n';
+         << ',' << t << ',' << hist << ',' << pairs << ',' << call.model_service_ms << ',' << ms << '\n';
     return live_ ? ms : call.model_service_ms;
   }
 
   void write(const std::string& dir) const {
     std::ofstream f(dir + "/forwards.csv");
-    f << "inst,kind,l_pad,depth,graph,members,tokens,model_ms,gpu_ms\n" << log_.str();
+    f << "inst,kind,l_pad,depth,graph,members,tokens,hist_tokens,attn_pairs,model_ms,gpu_ms\n" << log_.str();
     std::ofstream g(dir + "/first_tokens.csv");
     g << "req,token\n";
     std::vector<std::pair<RequestId, int32_t>> v(first_token_.begin(), first_token_.end());

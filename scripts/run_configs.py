@@ -19,7 +19,15 @@ from paper_2601_11589_b200 import engine as E  # noqa: E402
 from paper_2601_11589_b200 import scenarios as S  # noqa: E402
 from paper_2601_11589_b200.instance import MODELS, PrefillInstance  # noqa: E402
 
-PEAK_HBM, PEAK_TC = 6545.6e9, 1664.4e12
+def _peaks():
+    p = Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"] * 1e9, d["bf16_tflops"] * 1e12, d.get("bf16_tflops_sustained", d["bf16_tflops"]) * 1e12
+    return 6545.6e9, 1664.4e12, 1402.6e12
+
+
+PEAK_HBM, PEAK_TC, PEAK_TC_SUS = _peaks()
 
 CONFIGS = {
     "c1": ("tiny", S.DEFAULT, {}),
@@ -75,6 +83,19 @@ def main(names):
         gpu_s = st.gpu_ms_total / 1000.0
         live = E.simulate(cfg, "", d / "live", mode=E.LIVE, instances=[inst], token_seed=7)
         rows = list(csv.DictReader(open(d / "replay" / "forwards.csv")))
+        # Per-forward roofline: floor_i = max(bytes_i / HBM, flops_i / sustained bf16) from each
+        # dispatch's real tokens / histories; frac = sum floor / sum measured.
+        Vh = model.vocab * model.hidden
+        fl = {"graph": [0.0, 0.0], "standard": [0.0, 0.0], "all": [0.0, 0.0]}
+        for rw in rows:
+            T, Hs, pairs, n = int(rw["tokens"]), int(rw["hist_tokens"]), float(rw["attn_pairs"]), int(rw["members"])
+            b = model.weight_bytes + 2 * Vh + (T + Hs) * model.kv_bytes_per_token + T * model.hidden * 2
+            f = 2.0 * model.params_nonembed * T + 4.0 * model.n_q_heads * model.head_dim * model.layers * pairs + 2.0 * Vh * n
+            floor = max(b / PEAK_HBM, f / PEAK_TC_SUS)
+            t = float(rw["gpu_ms"]) * 1e-3
+            for k in ("graph" if rw["graph"] == "1" else "standard", "all"):
+                fl[k][0] += floor
+                fl[k][1] += t
         out[name] = {
             "model": mname, "requests": st.arrivals, "dispatches": st.dispatches, "gpu_forwards": st.gpu_forwards,
             "history_fills": st.fill_forwards, "gpu_seconds": gpu_s,
@@ -85,6 +106,7 @@ def main(names):
                      "slo_violation": live.slo_violation},
             "replay_cost_model": {"ttft_p50_ms": st.ttft_p50_ms, "ttft_p90_ms": st.ttft_p90_ms},
             "graph_forwards": sum(1 for r in rows if r["graph"] == "1"), "setup_s": setup,
+            "frac_roofline": {k: (v[0] / v[1] if v[1] else None) for k, v in fl.items()},
         }
         print(name, json.dumps(out[name]), flush=True)
         inst.close()
