@@ -17,9 +17,11 @@
 //            exchanged with the partner thread through smem (one named
 //            barrier per quarter per step), online softmax in the log2 domain
 //            with LAZY rescaling (the reference max moves only when a row max
-//            grows by > 2^8, so O in TMEM is rarely touched), P -> smem (bf16,
-//            128B swizzle); epilogue O / l -> bf16 (or fp32 partial for key
-//            splits).
+//            grows by > 2^8, so O in TMEM is rarely touched), P -> TMEM (bf16
+//            pairs; the PV MMA reads its A operand from tensor memory, so no
+//            smem round trip or async-proxy fence sits in the step);
+//            epilogue O / l -> bf16 (or fp32 partial for key splits).
+// TMEM (512 columns): S[2] 0 / 128, O 256, P 384 (64 packed columns).
 // Numerics match the mma.sync path (and the oracle's storage points): fp32
 // scores, bf16 P, fp32 O accumulation; key tiles of 128 instead of 64 change
 // only the online-softmax rescale points.
@@ -48,12 +50,11 @@ constexpr float kRescaleTau = 8.0f;  // log2 units: P <= 2^8 between rescales
 
 struct TcSmem {
   static constexpr int kQ = 0;
-  static constexpr int kP = kQ + kQBytes;
-  static constexpr int kK = kP + kQBytes;                 // [stage][32 KiB]
+  static constexpr int kK = kQ + kQBytes;                 // [stage][32 KiB]
   static constexpr int kV = kK + kKStages * kQBytes;      // [stage][32 KiB]
   static constexpr int kBars = kV + kVStages * kQBytes;
   static constexpr int kRed = kBars + 192;                // float [2 parity][2 group][128 rows]
-  static constexpr int kTotal = kRed + 2 * 2 * kRows * 4;  // 231,616 B of the 232,448 B limit
+  static constexpr int kTotal = kRed + 2 * 2 * kRows * 4;  // 198,848 B
 };
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -82,8 +83,8 @@ __device__ __forceinline__ uint32_t tile_addr(uint32_t base, int r, int c) {
 
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap kvm, const AttnCtx c) {
-  // No alignment slack fits beside 3 K stages: the dynamic window must start
-  // 1024-byte aligned (128B-swizzle atoms); trap loudly if it ever does not.
+  // The dynamic window must start 1024-byte aligned (128B-swizzle atoms);
+  // trap loudly if it ever does not.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t_end = partial ? wk.w : (p_hi + 1 + 63) / 64;  // one past the last page
   const int n_steps = (t_end - t_begin + 1) / 2;
 
-  const uint32_t sQ = smem_u32(smem + TcSmem::kQ), sP = smem_u32(smem + TcSmem::kP);
+  const uint32_t sQ = smem_u32(smem + TcSmem::kQ);
   const uint32_t sK = smem_u32(smem + TcSmem::kK), sV = smem_u32(smem + TcSmem::kV);
 
   if (warp == 0) {
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc_s = idesc_bf16(kRows, kKeys);
     constexpr uint32_t idesc_o = idesc_bf16(kRows, kD) | (1u << 16);  // B (V) is MN-major
     const uint32_t t_o = tmem + 2 * kKeys;
+    const uint32_t t_p = tmem + 3 * kKeys;  // P: 128 keys as 64 packed bf16x2 columns
     mbar_wait(q_ready, 0);
     tc_fence_after();
     auto issue_s = [&](int s) {
@@ -210,9 +212,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < kKeys / 16; ++k) {
-          const uint64_t a = sdesc_sw128(sP + (k >> 2) * kHalfBytes + (k & 3) * 32);
+          // P (A operand) straight from TMEM: 16 keys = 8 packed bf16x2 columns per MMA.
           const uint64_t b = sdesc_sw128_mn(sV + st * kQBytes + k * 16 * 128, kHalfBytes, 1024);
-          tc_mma_bf16(t_o, a, b, idesc_o, (s > 0 || k > 0) ? 1u : 0u);
+          tc_mma_bf16_ts(t_o, t_p + k * 8, b, idesc_o, (s > 0 || k > 0) ? 1u : 0u);
         }
         tc_commit(o_done);
         tc_commit(&v_empty[st]);
@@ -303,19 +305,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_wait_st();
         }
       }
-      // P half-row (bf16) -> smem: keys 0-63 are swizzle half 0, 64-127 half 1.
+      // P half-row (bf16 pairs) -> TMEM columns [grp*32, grp*32+32) of the P
+      // region (the PV MMA reads A from tensor memory: no smem round trip, no
+      // async-proxy fence).
+      {
+        const uint32_t t_pw = tmem + lane_off + 3 * kKeys + grp * 32;
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        uint4 w;
-        w.x = pack_bf16x2(sc[ch * 8 + 0], sc[ch * 8 + 1]);
-        w.y = pack_bf16x2(sc[ch * 8 + 2], sc[ch * 8 + 3]);
-        w.z = pack_bf16x2(sc[ch * 8 + 4], sc[ch * 8 + 5]);
-        w.w = pack_bf16x2(sc[ch * 8 + 6], sc[ch * 8 + 7]);
-        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(tile_addr(sP, rt, grp * 8 + ch)), "r"(w.x),
-                     "r"(w.y), "r"(w.z), "r"(w.w)
-                     : "memory");
+        for (int h = 0; h < 2; ++h) {
+          float w[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) w[i] = __uint_as_float(pack_bf16x2(sc[h * 32 + 2 * i], sc[h * 32 + 2 * i + 1]));
+          tmem_st16(t_pw + h * 16, w);
+        }
+        tc_wait_st();
       }
-      fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_ready);
