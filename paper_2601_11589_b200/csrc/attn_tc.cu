@@ -21,7 +21,9 @@
 //            pairs; the PV MMA reads its A operand from tensor memory, so no
 //            smem round trip or async-proxy fence sits in the step);
 //            epilogue O / l -> bf16 (or fp32 partial for key splits).
-// TMEM (512 columns): S[2] 0 / 128, O 256, P 384 (64 packed columns).
+// TMEM (512 columns): S[2] 0 / 128, O 256, P[2] 384 / 448 (64 packed columns
+// each; double-buffered, so softmax of step j+1 waits only for the PV two
+// steps back that read the same buffer).
 // Numerics match the mma.sync path (and the oracle's storage points): fp32
 // scores, bf16 P, fp32 O accumulation; key tiles of 128 instead of 64 change
 // only the online-softmax rescale points.
@@ -53,7 +55,7 @@ struct TcSmem {
   static constexpr int kK = kQ + kQBytes;                 // [stage][32 KiB]
   static constexpr int kV = kK + kKStages * kQBytes;      // [stage][32 KiB]
   static constexpr int kBars = kV + kVStages * kQBytes;
-  static constexpr int kRed = kBars + 192;                // float [2 parity][2 group][128 rows]
+  static constexpr int kRed = kBars + 256;                // float [2 parity][2 group][128 rows]
   static constexpr int kTotal = kRed + 2 * 2 * kRows * 4;  // 198,848 B
 };
 
@@ -95,9 +97,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* k_empty = bars + 21;   // [3]
   uint64_t* s_full = bars + 4;     // [2]
   uint64_t* s_empty = bars + 6;    // [2]
-  uint64_t* p_ready = bars + 8;
-  uint64_t* o_done = bars + 9;
+  uint64_t* p_ready = bars + 8;    // [2] P buffer written (8 softmax warps)
   uint64_t* q_ready = bars + 10;
+  uint64_t* p_free = bars + 24;    // [2] the PV that read the P buffer retired
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
   uint64_t* v_full = bars + 14;    // [2]
   uint64_t* v_empty = bars + 16;   // [2]
@@ -117,8 +119,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], kSoftmaxWarps);
     }
-    mbar_init(p_ready, kSoftmaxWarps);
-    mbar_init(o_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&p_ready[i], kSoftmaxWarps);
+      mbar_init(&p_free[i], 1);
+    }
     mbar_init(q_ready, kSoftmaxWarps);
     fence_mbar_init();
   }
@@ -181,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc_s = idesc_bf16(kRows, kKeys);
     constexpr uint32_t idesc_o = idesc_bf16(kRows, kD) | (1u << 16);  // B (V) is MN-major
     const uint32_t t_o = tmem + 2 * kKeys;
-    const uint32_t t_p = tmem + 3 * kKeys;  // P: 128 keys as 64 packed bf16x2 columns
+    const uint32_t t_p = tmem + 3 * kKeys;  // P[2]: 128 keys as 64 packed bf16x2 columns each
     mbar_wait(q_ready, 0);
     tc_fence_after();
     auto issue_s = [&](int s) {
@@ -202,11 +206,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     };
+    // S runs two steps ahead of PV: S(s+2) is queued right behind PV(s).
     if (n_steps > 0) issue_s(0);
+    if (n_steps > 1) issue_s(1);
     for (int s = 0; s < n_steps; ++s) {
       const int st = s & 1;
-      if (s + 1 < n_steps) issue_s(s + 1);
-      mbar_wait(p_ready, s & 1);
+      mbar_wait(&p_ready[st], (s >> 1) & 1);
       mbar_wait(&v_full[st], (s >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
@@ -214,12 +219,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < kKeys / 16; ++k) {
           // P (A operand) straight from TMEM: 16 keys = 8 packed bf16x2 columns per MMA.
           const uint64_t b = sdesc_sw128_mn(sV + st * kQBytes + k * 16 * 128, kHalfBytes, 1024);
-          tc_mma_bf16_ts(t_o, t_p + k * 8, b, idesc_o, (s > 0 || k > 0) ? 1u : 0u);
+          tc_mma_bf16_ts(t_o, t_p + st * 64 + k * 8, b, idesc_o, (s > 0 || k > 0) ? 1u : 0u);
         }
-        tc_commit(o_done);
+        tc_commit(&p_free[st]);
         tc_commit(&v_empty[st]);
       }
       __syncwarp();
+      if (s + 2 < n_steps) issue_s(s + 2);
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
@@ -288,11 +294,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       l_run = l_run * corr + sum;
 
-      // PV(s-1) must be complete before P is overwritten and O rescaled.
-      if (s > 0) {
-        mbar_wait(o_done, (s - 1) & 1);
+      // P buffer s&1 was read by PV(s-2); O may be rescaled only after every
+      // issued PV (up to s-1) retired (PVs retire in order).
+      if (s >= 2) {
+        mbar_wait(&p_free[s & 1], ((s >> 1) & 1) ^ 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, corr != 1.f)) {
+      }
+      if (s > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
+        mbar_wait(&p_free[(s - 1) & 1], ((s - 1) >> 1) & 1);
+        tc_fence_after();
+        {
           const uint32_t t_o = tmem + lane_off + 2 * kKeys + grp * (kD / 2);
 #pragma unroll 1
           for (int cc = 0; cc < kD / 32; ++cc) {
@@ -309,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // region (the PV MMA reads A from tensor memory: no smem round trip, no
       // async-proxy fence).
       {
-        const uint32_t t_pw = tmem + lane_off + 3 * kKeys + grp * 32;
+        const uint32_t t_pw = tmem + lane_off + 3 * kKeys + (s & 1) * 64 + grp * 32;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float w[16];
@@ -321,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_ready);
+      if (lane == 0) mbar_arrive(&p_ready[s & 1]);
     }
 
     // Epilogue: O row / l, l = both groups' partial sums (same reference max).
@@ -330,8 +341,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     st_shared_f32(lsum + (grp * kRows + rt) * 4, l_run);
     pair_sync();
     const float l_tot = l_run + ld_shared_f32(lsum + ((grp ^ 1) * kRows + rt) * 4);
-    if (n_steps > 0) {
-      mbar_wait(o_done, (n_steps - 1) & 1);
+    if (n_steps > 0) {  // the last PV retired
+      mbar_wait(&p_free[(n_steps - 1) & 1], ((n_steps - 1) >> 1) & 1);
       tc_fence_after();
     }
     const uint32_t t_o = tmem + lane_off + 2 * kKeys + grp * (kD / 2);
