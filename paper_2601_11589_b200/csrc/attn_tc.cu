@@ -5,7 +5,7 @@
 // One CTA = 128 packed (token, q-head) rows of one KV group x a key range.
 // Roles (192 threads):
 //   warp 0   TMA producers (lane 0 K, lane 1 V): pages (2 pages = 128 keys
-//            per step) into separate 2-stage K and V rings, laid out
+//            per step) into separate 3-stage K and V rings, laid out
 //            [d-half][128 keys][128 B] (128B swizzle);
 //   warp 1   MMA issuer (one thread):  S = Q K^T into TMEM (double-buffered,
 //            so S(j+1) overlaps the softmax of j), then O += P V with V as an
@@ -45,7 +45,7 @@ constexpr int kKeys = 128;                 // keys per step (2 pages)
 constexpr int kHalfBytes = kRows * 128;    // [128 rows][64 elems] bf16 = 16 KiB
 constexpr int kQBytes = 2 * kHalfBytes;    // Q / P / K / V tile: 32 KiB each
 constexpr int kKStages = 3;  // K runs a step further ahead (S(s+2) is issued right after PV(s))
-constexpr int kVStages = 2;
+constexpr int kVStages = 3;
 constexpr int kThreads = 320;
 constexpr int kSoftmaxWarps = 8;
 constexpr float kRescaleTau = 8.0f;  // log2 units: P <= 2^8 between rescales
@@ -56,7 +56,7 @@ struct TcSmem {
   static constexpr int kV = kK + kKStages * kQBytes;      // [stage][32 KiB]
   static constexpr int kBars = kV + kVStages * kQBytes;
   static constexpr int kRed = kBars + 256;                // float [2 parity][2 group][128 rows]
-  static constexpr int kTotal = kRed + 2 * 2 * kRows * 4;  // 198,848 B
+  static constexpr int kTotal = kRed + 2 * 2 * kRows * 4;  // 231,616 B of the 232,448 B limit
 };
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -101,8 +101,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* q_ready = bars + 10;
   uint64_t* p_free = bars + 24;    // [2] the PV that read the P buffer retired
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
-  uint64_t* v_full = bars + 14;    // [2]
-  uint64_t* v_empty = bars + 16;   // [2]
+  uint64_t* v_full = bars + 26;    // [3]
+  uint64_t* v_empty = bars + 29;   // [3]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   pdl_trigger();
@@ -113,9 +113,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kVStages; ++i) {
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], kSoftmaxWarps);
     }
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producers
-    // lane 0 streams K pages, lane 1 V pages (each into its own 2-stage ring).
+    // lane 0 streams K pages, lane 1 V pages (each into its own 3-stage ring).
     if (lane < 2) {
       const bool is_v = lane == 1;
       uint64_t* full = is_v ? v_full : k_full;
@@ -212,17 +214,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < n_steps; ++s) {
       const int st = s & 1;
       mbar_wait(&p_ready[st], (s >> 1) & 1);
-      mbar_wait(&v_full[st], (s >> 1) & 1);
+      const int vst = s % kVStages;
+      mbar_wait(&v_full[vst], (s / kVStages) & 1);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < kKeys / 16; ++k) {
           // P (A operand) straight from TMEM: 16 keys = 8 packed bf16x2 columns per MMA.
-          const uint64_t b = sdesc_sw128_mn(sV + st * kQBytes + k * 16 * 128, kHalfBytes, 1024);
+          const uint64_t b = sdesc_sw128_mn(sV + vst * kQBytes + k * 16 * 128, kHalfBytes, 1024);
           tc_mma_bf16_ts(t_o, t_p + st * 64 + k * 8, b, idesc_o, (s > 0 || k > 0) ? 1u : 0u);
         }
         tc_commit(&p_free[st]);
-        tc_commit(&v_empty[st]);
+        tc_commit(&v_empty[vst]);
       }
       __syncwarp();
       if (s + 2 < n_steps) issue_s(s + 2);
