@@ -140,6 +140,7 @@ Instance::Instance(const lp_model_desc& m, const lp_instance_desc& d) : m_(m), d
     fuse_resid_ = v == "1" || v == "resid";
   }
   if (const char* e = std::getenv("LP_GRAPH_ATTN_TC_MIN")) graph_tc_min_ = std::atoi(e);
+  if (const char* e = std::getenv("LP_GRAPH_TC_PAIRS")) graph_tc_pairs_ = std::atoll(e);
   if (const char* e = std::getenv("LP_ATTN_TC"); e && e[0] == '0') attn_tc_ = false;
   lp_check(cudaSetDevice(d.device), "cudaSetDevice");
   lp_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
@@ -575,7 +576,7 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
       int64_t pairs = 0;
       for (int i = 0; i < n; ++i) pairs += mem[i].new_tokens * (mem[i].history + mem[i].new_tokens);
       auto jt = graphs_tc_.find(graph_key(shape.l_pad, shape.depth));
-      if (attn_rows != kAttnTcRows && pairs >= kGraphTcPairs && jt != graphs_tc_.end()) {
+      if (attn_rows != kAttnTcRows && pairs >= graph_tc_pairs_ && jt != graphs_tc_.end()) {
         exec = jt->second;
         attn_rows = kAttnTcRows;
         tc_graph = true;

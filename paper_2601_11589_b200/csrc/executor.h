@@ -178,11 +178,11 @@ class Instance {
   // when no row block of the batch was split (every H = 0 batch, e.g.).
   std::map<int64_t, cudaGraphExec_t> graphs_nc_;
   // ... and a variant on the tcgen05 attention kernel, replayed when the
-  // batch's attention work sum_i L_i (H_i + L_i) reaches kGraphTcPairs (deep
+  // batch's attention work sum_i L_i (H_i + L_i) reaches graph_tc_pairs_ (deep
   // re-prefill buckets: measured 0.62 -> 0.68 of roofline at 256x4, H=1024;
   // the warp-MMA kernel stays faster for short rows).
   std::map<int64_t, cudaGraphExec_t> graphs_tc_;
-  static constexpr int64_t kGraphTcPairs = 500000;
+  int64_t graph_tc_pairs_ = 500000;  // LP_GRAPH_TC_PAIRS overrides
   bool submitted_ = false;
  public:
   size_t last_h2d_bytes_ = 0, last_d2h_bytes_ = 0;  // host<->device bytes of the last submit / read
