@@ -573,10 +573,16 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
       t_cap = static_cast<int>(shape.l_pad * shape.depth);
       r_cap = shape.depth;
       attn_rows = attn_rows_for(true, t_cap);
-      int64_t pairs = 0;
-      for (int i = 0; i < n; ++i) pairs += mem[i].new_tokens * (mem[i].history + mem[i].new_tokens);
+      int64_t pairs = 0, qtok = 0;
+      for (int i = 0; i < n; ++i) {
+        pairs += mem[i].new_tokens * (mem[i].history + mem[i].new_tokens);
+        qtok += mem[i].new_tokens;
+      }
+      // tcgen05 pays off for long key ranges (mean keys per query >= 512,
+      // i.e. re-prefills over histories) with enough total work; short causal
+      // blocks (H = 0) stay on the warp-MMA kernel.
       auto jt = graphs_tc_.find(graph_key(shape.l_pad, shape.depth));
-      if (attn_rows != kAttnTcRows && pairs >= graph_tc_pairs_ && jt != graphs_tc_.end()) {
+      if (attn_rows != kAttnTcRows && pairs >= graph_tc_pairs_ && pairs >= 512 * qtok && jt != graphs_tc_.end()) {
         exec = jt->second;
         attn_rows = kAttnTcRows;
         tc_graph = true;

@@ -178,7 +178,8 @@ class Instance {
   // when no row block of the batch was split (every H = 0 batch, e.g.).
   std::map<int64_t, cudaGraphExec_t> graphs_nc_;
   // ... and a variant on the tcgen05 attention kernel, replayed when the
-  // batch's attention work sum_i L_i (H_i + L_i) reaches graph_tc_pairs_ (deep
+  // batch's attention work sum_i L_i (H_i + L_i) reaches graph_tc_pairs_ with
+  // >= 512 keys per query on average (deep
   // re-prefill buckets: measured 0.62 -> 0.68 of roofline at 256x4, H=1024;
   // the warp-MMA kernel stays faster for short rows).
   std::map<int64_t, cudaGraphExec_t> graphs_tc_;
