@@ -105,7 +105,12 @@ int lp_instance_destroy(lp_instance* inst);
 /* Model descriptor the instance was created with. */
 int lp_instance_model(lp_instance* inst, lp_model_desc* out);
 /* Capture graphs for every (length, depth) of the grid — GraphGrid,
- * scheduler.hpp:21-32. No-op when use_graphs == 0. */
+ * scheduler.hpp:21-32 — plus per-64-token chunk graphs (up to C_l = 512,
+ * scheduler.hpp:46) for one-member standard launches. Each grid shape gets
+ * variants chosen per batch at lp_submit (attention merge grid or not,
+ * warp-MMA or tcgen05 attention); replays read every live size from device
+ * metadata, so no variant depends on the histories. No-op when
+ * use_graphs == 0. */
 int lp_capture_graphs(lp_instance* inst, const int64_t* lengths, int32_t n_lengths,
                       const int32_t* depths, int32_t n_depths);
 
