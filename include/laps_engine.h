@@ -56,6 +56,15 @@ typedef struct lp_sim_stats {
 int lp_sim_run(const char* cfg_text, const char* overrides, const char* out_dir, int32_t mode,
                lp_instance** insts, int32_t n_insts, uint64_t token_seed, lp_sim_stats* stats);
 
+/* The reference CLI's `prefillsim sweep --param P --values v1,v2,...`
+ * (tools/main.cpp:114-168): for each value (sorted ascending) apply
+ * apply_sweep_param (config.cpp:353-372) to a fresh copy of the config, run the
+ * engine in `mode` (cost model, or on the GPU instances), and write
+ * out_dir/sweep.csv with the reference's columns and number formats. */
+int lp_sim_sweep(const char* cfg_text, const char* overrides, const char* out_dir, int32_t mode,
+                 lp_instance** insts, int32_t n_insts, uint64_t token_seed, const char* param,
+                 const char* values_csv);
+
 /* Dump the scenario's request stream as text lines
  * "id session turn L H arrival(%.17g) deadline(%.17g|none)". */
 int lp_sim_trace(const char* cfg_text, const char* overrides, const char* path);

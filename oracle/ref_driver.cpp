@@ -13,6 +13,8 @@
 //                    config.cpp:337) as text for the host-engine parity tests.
 //   ref_service_ms — batch_service_time (cost_model.cpp:128-148).
 //   ref_acceptance — run_acceptance (acceptance.cpp:899-928).
+//   ref_sweep      — the CLI's `sweep` (tools/main.cpp:114-168) restated on
+//                    the library's apply_sweep_param / run_scenario.
 //
 // Nothing in the product path loads this library.
 #include <prefillsim/acceptance.hpp>
@@ -22,7 +24,9 @@
 #include <prefillsim/metrics.hpp>
 #include <prefillsim/sim.hpp>
 
+#include <algorithm>
 #include <chrono>
+#include <vector>
 #include <cinttypes>
 #include <cstdio>
 #include <cstring>
@@ -126,6 +130,65 @@ int ref_acceptance() {
     bad += r.pass ? 0 : 1;
   }
   return bad;
+}
+
+// ref_sweep — restates the reference CLI's `sweep` subcommand
+// (tools/main.cpp:114-168; the CLI itself needs CLI11, absent here) on top of
+// the reference library's apply_sweep_param / build_scenario / run_scenario
+// (config.cpp:353-378): same value order, columns and printf formats.
+int ref_sweep(const char* cfg_text, const char* overrides, const char* out_dir, const char* param,
+              const char* values_csv) {
+  try {
+    const ConfigMap base = make_map(cfg_text, overrides);
+    std::vector<double> values;
+    std::stringstream ss(values_csv ? values_csv : "");
+    std::string item;
+    while (std::getline(ss, item, ',')) {
+      if (item.empty()) continue;
+      values.push_back(std::stod(item));
+    }
+    if (values.empty()) throw std::runtime_error("empty values");
+    std::sort(values.begin(), values.end());
+    auto cls = [](std::string& row, const ClassMetrics& c) {
+      char buf[256];
+      std::snprintf(buf, sizeof buf, ",%lld,%.6f,%.6f,%.6f,%.6f,%.6f,%.6f,%.6f,%lld,%.6f,%.6f,%.6f",
+                    static_cast<long long>(c.completed), c.ttft_mean_ms, c.ttft_p50_ms, c.ttft_p90_ms,
+                    c.ttft_p99_ms, c.rps, c.slo_violation, c.mean_wait_ms, static_cast<long long>(c.batches),
+                    c.mean_depth, c.graph_hit_rate, c.padding_overhead);
+      row += buf;
+    };
+    const char* cols_all =
+        "completed,ttft_mean_ms,ttft_p50_ms,ttft_p90_ms,ttft_p99_ms,rps,slo_violation,mean_wait_ms,batches,"
+        "mean_depth,graph_hit_rate,padding_overhead";
+    std::string csv = "param,value,arrivals,active_ms,migrations";
+    for (const char* scope : {"overall_", "short_", "long_"}) {
+      std::stringstream cols(cols_all);
+      std::string col;
+      while (std::getline(cols, col, ',')) csv += std::string(",") + scope + col;
+    }
+    csv += '\n';
+    for (double v : values) {
+      ConfigMap cfg = base;
+      apply_sweep_param(cfg, param, v);
+      const RunResult rr = run_scenario(build_scenario(cfg));
+      char head[160];
+      std::snprintf(head, sizeof head, "%s,%.6f,%lld,%.6f,%lld", param, v,
+                    static_cast<long long>(rr.report.arrivals), rr.report.active_ms,
+                    static_cast<long long>(rr.report.migrations));
+      std::string row = head;
+      cls(row, rr.report.overall);
+      cls(row, rr.report.short_cls);
+      cls(row, rr.report.long_cls);
+      csv += row + '\n';
+    }
+    std::filesystem::create_directories(out_dir);
+    std::ofstream os(std::string(out_dir) + "/sweep.csv", std::ios::binary);
+    os << csv;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
 }
 
 }  // extern "C"

@@ -77,7 +77,7 @@ PUBLIC_SYMBOLS = [
     "lp_read_kv", "lp_session_migrate", "lp_synth_token", "lp_last_error", "lp_version",
     "lp_instance_model", "lp_timer_record", "lp_timer_elapsed", "lp_last_io", "lp_last_launches",
 ]
-ENGINE_SYMBOLS = ["lp_sim_run", "lp_sim_trace"]  # include/laps_engine.h
+ENGINE_SYMBOLS = ["lp_sim_run", "lp_sim_trace", "lp_sim_sweep"]  # include/laps_engine.h
 
 
 def _declare(L: ctypes.CDLL) -> None:

@@ -13,6 +13,7 @@
 #include <cinttypes>
 #include <cstdio>
 #include <filesystem>
+#include <memory>
 #include <fstream>
 #include <sstream>
 #include <unordered_map>
@@ -98,6 +99,14 @@ class GpuBackend final : public ForwardBackend {
     for (auto& [r, t] : v) g << r << ',' << t << '\n';
   }
 
+  // Sessions still resident when the run ends (their last turn did not
+  // finish inside the simulated window) are released, so an instance reused
+  // for the next run (sweeps, repeated benchmarks) starts from an empty pool:
+  // session ids restart at 0 in every workload.
+  ~GpuBackend() override {
+    for (const auto& [sid, gi] : owner_) lp_session_release(insts_[static_cast<size_t>(gi)], sid);
+  }
+
   lp_sim_stats stats_{};
 
  private:
@@ -150,10 +159,39 @@ class GpuBackend final : public ForwardBackend {
   std::ostringstream log_;
 };
 
-Scenario scenario_from(const char* cfg_text, const char* overrides) {
+ConfigMap config_from(const char* cfg_text, const char* overrides) {
   ConfigMap cfg = parse_config_text(cfg_text ? cfg_text : "");
   if (overrides && *overrides) apply_overrides(cfg, parse_config_text(overrides));
-  return build_scenario(cfg);
+  return cfg;
+}
+
+Scenario scenario_from(const char* cfg_text, const char* overrides) {
+  return build_scenario(config_from(cfg_text, overrides));
+}
+
+// One engine run: closed-form service times, or every dispatch on the GPU
+// instances (replay: cost-model clock; live: measured clock).
+RunResult run_mode(const Scenario& sc, int32_t mode, lp_instance** insts, int32_t n_insts, uint64_t token_seed,
+                   std::unique_ptr<GpuBackend>* keep) {
+  const std::vector<Request> reqs = build_workload(sc);
+  if (mode == LP_SIM_COST_MODEL) return run(sc.sim, reqs, sc.cost, sc.overheads, sc.sched, sc.grid, sc.ctrl);
+  if (!insts || n_insts < 1) throw ConfigError("GPU modes need at least one instance");
+  lp_model_desc md{};
+  check(lp_instance_model(insts[0], &md), "lp_instance_model");
+  auto gpu = std::make_unique<GpuBackend>(insts, n_insts, mode == LP_SIM_LIVE, token_seed, md.vocab, reqs);
+  RunResult rr = run_with_backend(sc.sim, reqs, sc.cost, sc.overheads, sc.sched, sc.grid, sc.ctrl, *gpu);
+  if (keep) *keep = std::move(gpu);
+  return rr;
+}
+
+// sweep.csv row columns of the reference CLI (tools/main.cpp:97-113).
+void csv_class(std::string& row, const ClassMetrics& c) {
+  char buf[256];
+  std::snprintf(buf, sizeof buf, ",%lld,%.6f,%.6f,%.6f,%.6f,%.6f,%.6f,%.6f,%lld,%.6f,%.6f,%.6f",
+                static_cast<long long>(c.completed), c.ttft_mean_ms, c.ttft_p50_ms, c.ttft_p90_ms, c.ttft_p99_ms,
+                c.rps, c.slo_violation, c.mean_wait_ms, static_cast<long long>(c.batches), c.mean_depth,
+                c.graph_hit_rate, c.padding_overhead);
+  row += buf;
 }
 
 }  // namespace
@@ -171,20 +209,10 @@ int lp_sim_run(const char* cfg_text, const char* overrides, const char* out_dir,
   try {
     const auto t0 = std::chrono::steady_clock::now();
     const Scenario sc = scenario_from(cfg_text, overrides);
-    const std::vector<Request> reqs = build_workload(sc);
-    RunResult rr;
     lp_sim_stats st{};
     std::unique_ptr<GpuBackend> gpu;
-    if (mode == LP_SIM_COST_MODEL) {
-      rr = run(sc.sim, reqs, sc.cost, sc.overheads, sc.sched, sc.grid, sc.ctrl);
-    } else {
-      if (!insts || n_insts < 1) throw ConfigError("GPU modes need at least one instance");
-      lp_model_desc md{};
-      check(lp_instance_model(insts[0], &md), "lp_instance_model");
-      gpu = std::make_unique<GpuBackend>(insts, n_insts, mode == LP_SIM_LIVE, token_seed, md.vocab, reqs);
-      rr = run_with_backend(sc.sim, reqs, sc.cost, sc.overheads, sc.sched, sc.grid, sc.ctrl, *gpu);
-      st = gpu->stats_;
-    }
+    RunResult rr = run_mode(sc, mode, insts, n_insts, token_seed, &gpu);
+    if (gpu) st = gpu->stats_;
     if (out_dir && *out_dir) {
       std::filesystem::create_directories(out_dir);
       write_event_log(std::string(out_dir) + "/events.log", rr.log);
@@ -210,6 +238,60 @@ int lp_sim_run(const char* cfg_text, const char* overrides, const char* out_dir,
   } catch (const laps::ShapeMismatch& e) {
     lp::set_last_error(e.what());
     return LP_ERR_SHAPE;
+  } catch (const laps::ConfigError& e) {
+    lp::set_last_error(e.what());
+    return LP_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    lp::set_last_error(e.what());
+    return LP_ERR_INTERNAL;
+  }
+}
+
+int lp_sim_sweep(const char* cfg_text, const char* overrides, const char* out_dir, int32_t mode,
+                 lp_instance** insts, int32_t n_insts, uint64_t token_seed, const char* param,
+                 const char* values_csv) {
+  using namespace laps;
+  try {
+    if (!param || !*param) throw ConfigError("sweep: empty parameter name");
+    const ConfigMap base = config_from(cfg_text, overrides);
+    std::vector<double> values;
+    std::stringstream ss(values_csv ? values_csv : "");
+    std::string item;
+    while (std::getline(ss, item, ',')) {
+      if (item.empty()) continue;
+      values.push_back(std::stod(item));
+    }
+    if (values.empty()) throw ConfigError("sweep: --values parsed to an empty list");
+    std::sort(values.begin(), values.end());
+    static const char* kClassCols =
+        "completed,ttft_mean_ms,ttft_p50_ms,ttft_p90_ms,ttft_p99_ms,rps,slo_violation,mean_wait_ms,batches,"
+        "mean_depth,graph_hit_rate,padding_overhead";
+    std::string csv = "param,value,arrivals,active_ms,migrations";
+    for (const char* scope : {"overall_", "short_", "long_"}) {
+      std::stringstream cols(kClassCols);
+      std::string col;
+      while (std::getline(cols, col, ',')) csv += std::string(",") + scope + col;
+    }
+    csv += '\n';
+    for (double v : values) {
+      ConfigMap cfg = base;  // fresh copy: scaling params read base values
+      apply_sweep_param(cfg, param, v);
+      const RunResult rr = run_mode(build_scenario(cfg), mode, insts, n_insts, token_seed, nullptr);
+      char head[160];
+      std::snprintf(head, sizeof head, "%s,%.6f,%lld,%.6f,%lld", param, v,
+                    static_cast<long long>(rr.report.arrivals), rr.report.active_ms,
+                    static_cast<long long>(rr.report.migrations));
+      std::string row = head;
+      csv_class(row, rr.report.overall);
+      csv_class(row, rr.report.short_cls);
+      csv_class(row, rr.report.long_cls);
+      csv += row + '\n';
+    }
+    std::filesystem::create_directories(out_dir);
+    std::ofstream os(std::string(out_dir) + "/sweep.csv", std::ios::binary);
+    if (!os) throw std::runtime_error("sweep: cannot write sweep.csv");
+    os << csv;
+    return LP_OK;
   } catch (const laps::ConfigError& e) {
     lp::set_last_error(e.what());
     return LP_ERR_CONFIG;

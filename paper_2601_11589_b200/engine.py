@@ -37,10 +37,31 @@ def _declare():
         L.lp_sim_run.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int32,
                                  ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, ctypes.c_uint64,
                                  ctypes.POINTER(SimStats)]
+        L.lp_sim_sweep.restype = ctypes.c_int32
+        L.lp_sim_sweep.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int32,
+                                   ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, ctypes.c_uint64,
+                                   ctypes.c_char_p, ctypes.c_char_p]
         L.lp_sim_trace.restype = ctypes.c_int32
         L.lp_sim_trace.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p]
         L._engine_declared = True
     return L
+
+
+def sweep(config_text: str, param: str, values, out_dir: str | Path, overrides: str | dict = "",
+          mode: int = COST_MODEL, instances: list[PrefillInstance] | None = None, token_seed: int = 7) -> Path:
+    """The reference CLI's `prefillsim sweep` (tools/main.cpp:114-168): one
+    engine run per value of `param` (apply_sweep_param semantics, e.g.
+    "short_concurrency" scales workload.lambda_per_ms), in cost-model mode or
+    on GPU instances; returns the path of sweep.csv."""
+    if isinstance(overrides, dict):
+        overrides = "".join(f"{k} = {v}\n" for k, v in overrides.items())
+    L = _declare()
+    insts = instances or []
+    arr = (ctypes.c_void_p * max(1, len(insts)))(*[i._h.value for i in insts])
+    vals = ",".join(repr(float(v)) for v in values)
+    N.check(L.lp_sim_sweep(config_text.encode(), overrides.encode(), str(out_dir).encode(), mode,
+                           arr if insts else None, len(insts), token_seed, param.encode(), vals.encode()))
+    return Path(out_dir) / "sweep.csv"
 
 
 def read_config(path: str | Path) -> str:
