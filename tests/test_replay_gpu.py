@@ -73,3 +73,36 @@ def test_sampled_first_tokens_match_oracle(replay):
                 assert first[r.id] == int(torch.argmax(logits)), f"req {r.id}"
                 checked += 1
     assert checked >= 6
+
+
+def test_spatial_two_instances_migrate_session_kv(tmp_path):
+    """Spatial disaggregation across two prefill instances (same GPU here;
+    NVLink peer reads across GPUs): re-prefills that land on the other
+    instance move their session KV (lp_session_migrate's page-gather
+    kernel); composition stays byte-identical and the migrated sessions'
+    first tokens match the oracle."""
+    insts = [PrefillInstance(TINY, max_tokens=8192, max_members=64, kv_pages=20000) for _ in range(2)]
+    for i in insts:
+        i.capture_graphs()
+    out = tmp_path / "spatial2"
+    st = E.simulate(S.text(S.DEFAULT), "", out, mode=E.REPLAY, instances=insts, token_seed=7)
+    assert hashlib.sha256((out / "events.log").read_bytes()).hexdigest() == GOLD["default"]["events_sha256"]
+    assert st.kv_migrations > 100  # ~58% of later turns change instance (SURVEY.md §0.6)
+    E.dump_trace(S.text(S.DEFAULT), "", out / "trace.txt")
+    trace = E.load_trace_dump(out / "trace.txt")
+    first = {int(r["req"]): int(r["token"]) for r in csv.DictReader(open(out / "first_tokens.csv"))}
+    by_session = {}
+    for r in trace:
+        by_session.setdefault(r.session, []).append(r)
+    checked = 0
+    for sid in [s for s, rs in by_session.items() if len(rs) >= 3][:5]:
+        o = FO.OracleModel(FO.TINY)
+        for r in sorted(by_session[sid], key=lambda r: r.turn):
+            logits = o.forward([(r.session, r.L, r.H)], [FO.tokens(7, r.session, r.H, r.L, TINY.vocab)])[0]
+            top2 = torch.topk(logits, 2).values
+            if (top2[0] - top2[1]).item() > 4e-2:
+                assert first[r.id] == int(torch.argmax(logits)), f"req {r.id}"
+                checked += 1
+    assert checked >= 5
+    for i in insts:
+        i.close()
