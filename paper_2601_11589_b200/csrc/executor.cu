@@ -161,6 +161,7 @@ Instance::~Instance() {
   for (auto& [k, g] : chunk_graphs_) cudaGraphExecDestroy(g);
   for (void* p : allocs_) cudaFree(p);
   if (meta_host_) cudaFreeHost(meta_host_);
+  if (mig_host_) cudaFreeHost(mig_host_);
   cudaEventDestroy(ev_start_);
   cudaEventDestroy(ev_end_);
   cudaEventDestroy(ev_h2d_);
@@ -262,6 +263,9 @@ void Instance::alloc_arena() {
   layer_stride_ = page_elems_ * size_t(n_pages_);
   kv_pool_ = dmalloc<bf16>(layer_stride_ * m_.layers, allocs_);
   for (int32_t p = 0; p < n_pages_; ++p) free_pages_.insert(free_pages_.end(), p);
+  // Page-id lists of an incoming session migration (source ids, then ours).
+  mig_ids_ = dmalloc<int>(size_t(2) * n_pages_, allocs_);
+  lp_check(cudaMallocHost(reinterpret_cast<void**>(&mig_host_), size_t(2) * n_pages_ * sizeof(int)), "pinned ids");
   tm_kv_ = make_kv_tmap(kv_pool_, int64_t(m_.layers) * n_pages_ * 2 * m_.n_kv_heads, D);
   // Key-range split partials: only the first kAttnSplitCap work items may be partial.
   // Eager launches (long chunks, off-grid / packed batches: long key ranges,
@@ -876,18 +880,18 @@ void Instance::migrate(Instance& src, Instance& dst, int64_t sid) {
   if (peer) {
     // One kernel on the destination: reads the source pool directly (same
     // HBM, or the peer's HBM over NVLink) and writes the new pages.
-    int* ids = nullptr;
-    lp_check(cudaMallocAsync(reinterpret_cast<void**>(&ids), size_t(2) * n * sizeof(int), dst.stream_), "ids");
-    std::vector<int> h(2 * n);
+    // Page ids travel through the destination's pinned staging buffer (the
+    // sync below keeps it alive until the copy has read them).
+    int* h = dst.mig_host_;
     for (int k = 0; k < n; ++k) {
       h[k] = ss.pages[k];
       h[n + k] = ds.pages[k];
     }
-    lp_check(cudaMemcpyAsync(ids, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, dst.stream_), "ids h2d");
+    int* ids = dst.mig_ids_;
+    lp_check(cudaMemcpyAsync(ids, h, size_t(2) * n * sizeof(int), cudaMemcpyHostToDevice, dst.stream_), "ids h2d");
     kv_page_copy(src.kv_pool_, src.layer_stride_, dst.kv_pool_, dst.layer_stride_, src.page_elems_, ids, ids + n, n,
                  src.m_.layers, dst.stream_);
     lp_check(cudaGetLastError(), "kv copy");
-    lp_check(cudaFreeAsync(ids, dst.stream_), "ids free");
   } else {
     const size_t bytes = src.page_elems_ * 2;
     for (int l = 0; l < src.m_.layers; ++l) {

@@ -144,6 +144,8 @@ class Instance {
   unsigned long long* next_keys_ = nullptr;
   void* meta_dev_ = nullptr;
   void* meta_host_ = nullptr;
+  int* mig_ids_ = nullptr;   // device page-id lists of an incoming migration
+  int* mig_host_ = nullptr;  // pinned staging for them
   size_t meta_bytes_ = 0;
   Meta md_{}, mh_{};
   std::map<std::tuple<const void*, int, int>, CUtensorMap> act_maps_;

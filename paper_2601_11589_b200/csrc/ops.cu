@@ -316,7 +316,22 @@ __global__ void kv_page_copy_kernel(const uint4* __restrict__ src_pool, size_t s
   const int k = blockIdx.x, l = blockIdx.y;
   const uint4* s = src_pool + l * src_layer_stride + static_cast<size_t>(src_pages[k]) * page_vec;
   uint4* d = dst_pool + l * dst_layer_stride + static_cast<size_t>(dst_pages[k]) * page_vec;
-  for (size_t i = threadIdx.x; i < page_vec; i += blockDim.x) d[i] = s[i];
+  // All of a thread's loads in flight before its stores; streaming hints:
+  // the pages are not re-read by this kernel.
+  constexpr int kU = 4;
+  for (size_t base = threadIdx.x; base < page_vec; base += size_t(blockDim.x) * kU) {
+    uint4 r[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const size_t i = base + size_t(u) * blockDim.x;
+      if (i < page_vec) r[u] = __ldcs(s + i);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const size_t i = base + size_t(u) * blockDim.x;
+      if (i < page_vec) __stcs(d + i, r[u]);
+    }
+  }
 }
 
 void kv_page_copy(const bf16* src_pool, size_t src_layer_stride, bf16* dst_pool, size_t dst_layer_stride,
