@@ -304,6 +304,7 @@ CUtensorMap make_kv_tmap(const void* pool, int64_t planes, int head_dim) {
 
 void attention_prefill(const AttnCtx& c, const CUtensorMap& kv_map, int head_dim, int work_cap,
                        int combine_cap, cudaStream_t st, bool with_combine) {
+  if (debug_empty("attn")) return launch_empty(dim3(work_cap), dim3(128), st);
   if (head_dim == 128 && c.block_rows == kAttnTcRows) {
     attention_prefill_tc(c, kv_map, work_cap, st);
   } else if (head_dim == 128) {

@@ -1,5 +1,6 @@
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -760,7 +761,14 @@ double Instance::time_gemm(int layer, int which, int t_cap, int n_live, int iter
   mh_.scalars[1] = std::min(n_live, r_max_);
   GemmPlan pl = *p;
   if (g.mode != kEpiF32Partial) pl.s_cap = 1;
-  const TilePlan tp = choose_tiles(g.M, g.K, pl, n_live, num_sms());
+  TilePlan tp = choose_tiles(g.M, g.K, pl, n_live, num_sms());
+  if (const char* e = std::getenv("LP_TIME_GEMM_PLAN")) {  // experiments: "n_tiles,splits"
+    int nt = 0, s = 0;
+    if (std::sscanf(e, "%d,%d", &nt, &s) == 2 && nt >= 1 && nt <= pl.nt_cap && s >= 1 && s <= std::max(1, pl.s_cap)) {
+      tp.n_tiles = nt;
+      tp.splits = s;
+    }
+  }
   mh_.scalars[4] = tp.splits;
   mh_.scalars[8] = tp.n_tiles;
   g.ntiles_dev = md_.scalars + 8;

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 
 namespace lp {
 
@@ -42,5 +43,15 @@ cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
+
+// Timing experiments only (results are wrong): LP_DEBUG_EMPTY lists kernel
+// classes ("norm", "qkv", "attn") whose launches are replaced by an empty PDL
+// kernel of the same grid, to split a forward's time into kernel work and
+// kernel-boundary cost.
+inline bool debug_empty(const char* cls) {
+  const char* e = std::getenv("LP_DEBUG_EMPTY");
+  return e && std::strstr(e, cls) != nullptr;
+}
+void launch_empty(dim3 grid, dim3 block, cudaStream_t st);
 
 }  // namespace lp

@@ -355,8 +355,16 @@ void embed_rmsnorm(const RowCtx& c, const int* tokens, const bf16* embed, const 
            x_resid, x_norm);
 }
 
+__global__ void pdl_empty_kernel() {
+  pdl_trigger();
+  pdl_wait();
+}
+
+void launch_empty(dim3 grid, dim3 block, cudaStream_t st) { launch_k(pdl_empty_kernel, grid, block, 0, st); }
+
 void resid_rmsnorm(const RowCtx& c, const float* ws, int splits, const int* splits_dev, size_t ws_stride_rows,
                    float* x_resid, const bf16* gamma, bf16* x_norm, cudaStream_t st) {
+  if (debug_empty("norm")) return launch_empty(dim3(c.t_cap), dim3(kRowThreads), st);
   launch_k(resid_rmsnorm_kernel, dim3(c.t_cap), dim3(kRowThreads), 0, st, c, ws, splits, splits_dev,
            ws_stride_rows, x_resid, gamma, x_norm);
 }
@@ -383,6 +391,7 @@ void qkv_post(const QkvCtx& c, cudaStream_t st) {
     return threads <= cap;
   };
   const bool deep = c.s_cap > 2;
+  if (debug_empty("qkv")) return launch_empty(dim3(c.t_cap), dim3(threads_for(deep ? 1 : 4)), st);
   if (deep && fits(reinterpret_cast<const void*>(qkv_post_kernel<1, 8>), threads_for(1))) {
     launch_k(qkv_post_kernel<1, 8>, dim3(c.t_cap), dim3(threads_for(1)), 0, st, c);
   } else if (deep && fits(reinterpret_cast<const void*>(qkv_post_kernel<2, 4>), threads_for(2))) {
