@@ -64,13 +64,14 @@ def main():
                         "note": "bench.py default run: most common step capacity 4096, median live tokens 2846"}]
     (P / "r01_dominant_kernel.json").write_text(json.dumps(dom, indent=1))
     tags = ["7b_16x1", "7b_16x1_h1024", "7b_64x4_h1024", "7b_256x1", "7b_chunk512_h1536", "7b_256x16", "32b_16x1",
-            "32b_chunk512_h1536"]
+            "32b_chunk512_h1536", "7b_8x64_h4000", "7b_16x16_h4000"]
     nf = json.loads((P / "r01_ncu_forwards.json").read_text())
     nf["forwards"] = {t: json.load(open(G / f"ncu_fwd_{t}.json")) for t in tags}
     (P / "r01_ncu_forwards.json").write_text(json.dumps(nf, indent=1))
     names = {"7b_16x1": "7B 16x1, H=0", "7b_16x1_h1024": "7B 16x1, H=1024", "7b_64x4_h1024": "7B 64x4, H=1024",
              "7b_256x1": "7B 256x1, H=0", "7b_chunk512_h1536": "7B 512-token chunk, H=1536",
-             "7b_256x16": "7B 256x16, H=0", "32b_16x1": "32B 16x1, H=0", "32b_chunk512_h1536": "32B 512-token chunk, H=1536"}
+             "7b_256x16": "7B 256x16, H=0", "32b_16x1": "32B 16x1, H=0", "32b_chunk512_h1536": "32B 512-token chunk, H=1536",
+             "7b_8x64_h4000": "7B 8x64, H=4000", "7b_16x16_h4000": "7B 16x16, H=4000"}
     ncu_rows = []
     for t in tags:
         d = nf["forwards"][t]
@@ -83,7 +84,8 @@ def main():
               bucket_table(P / "r01_buckets_7b_h1024.json", "Qwen2.5-7B re-prefill, H=1024 per member") + "\n" +
               bucket_table(P / "r01_buckets_32b_h0.json", "Qwen2.5-32B, H=0") + "\n")
     s = (P / "r01_summary.md").read_text()
-    i, j = s.index("**Qwen2.5-7B, H=0**"), s.index("## BASELINE configs on one B200")
+    # Generated bucket tables end where the hand-written KV-dominated section starts.
+    i, j = s.index("**Qwen2.5-7B, H=0**"), s.index("**Qwen2.5-7B, KV-dominated re-prefill")
     s = s[:i] + tables + "\n" + s[j:]
     i = s.index("| 7B 16x1, H=0 |")
     j = s.index("\n\n", i)
