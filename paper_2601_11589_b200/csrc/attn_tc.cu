@@ -27,6 +27,7 @@
 // Numerics match the mma.sync path (and the oracle's storage points): fp32
 // scores, bf16 P, fp32 O accumulation; key tiles of 128 instead of 64 change
 // only the online-softmax rescale points.
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 
@@ -82,6 +83,23 @@ __device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gmem)
 __device__ __forceinline__ uint32_t tile_addr(uint32_t base, int r, int c) {
   return base + (c >> 3) * kHalfBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4);
 }
+
+// Diagnostic build only (-DLP_ATTN_PROF, scripts/attn_prof.py): clock64
+// stamps per step for the MMA issuer, one softmax warp and the K producer of
+// the first kProfCtas CTAs of KV head 0. Compiled out of the product library.
+#ifdef LP_ATTN_PROF
+constexpr int kProfCtas = 128, kProfSteps = 64;
+__device__ unsigned long long g_attn_prof[kProfCtas][3][kProfSteps][4];
+#define ATTN_PROF(role, step, ev)                                                            \
+  do {                                                                                       \
+    if (blockIdx.y == 0 && blockIdx.x < kProfCtas && (step) < kProfSteps && (step) >= 0)     \
+      g_attn_prof[blockIdx.x][role][step][ev] = clock64();                                   \
+  } while (0)
+#else
+#define ATTN_PROF(role, step, ev) \
+  do {                            \
+  } while (0)
+#endif
 
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap kvm, const AttnCtx c) {
@@ -168,7 +186,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ns = is_v ? kVStages : kKStages;
       for (int s = 0; s < n_steps; ++s) {
         const int st = s % ns;
+        if (!is_v) ATTN_PROF(2, s, 0);
         mbar_wait(&empty[st], ((s / ns) & 1) ^ 1);
+        if (!is_v) ATTN_PROF(2, s, 1);
         mbar_arrive_expect_tx(&full[st], kQBytes);
         const int t0 = t_begin + 2 * s;
         // A missing second page re-loads the first (finite values, masked).
@@ -213,9 +233,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (n_steps > 1) issue_s(1);
     for (int s = 0; s < n_steps; ++s) {
       const int st = s & 1;
+      if (lane == 0) ATTN_PROF(0, s, 0);
       mbar_wait(&p_ready[st], (s >> 1) & 1);
+      if (lane == 0) ATTN_PROF(0, s, 1);
       const int vst = s % kVStages;
       mbar_wait(&v_full[vst], (s / kVStages) & 1);
+      if (lane == 0) ATTN_PROF(0, s, 2);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -229,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
       if (s + 2 < n_steps) issue_s(s + 2);
+      if (lane == 0) ATTN_PROF(0, s, 3);
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
@@ -255,7 +279,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m_run = -INFINITY, l_run = 0.f;  // l_run: this thread's columns only
     for (int s = 0; s < n_steps; ++s) {
       const int st = s & 1;
+      const bool prof_me = warp == 2 && lane == 0;
+      if (prof_me) ATTN_PROF(1, s, 0);
       mbar_wait(&s_full[st], (s >> 1) & 1);
+      if (prof_me) ATTN_PROF(1, s, 1);
       tc_fence_after();
       float sc[kHalf];
 #pragma unroll
@@ -296,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         sum += sc[k];
       }
       l_run = l_run * corr + sum;
+      if (prof_me) ATTN_PROF(1, s, 2);
 
       // P buffer s&1 was read by PV(s-2); O may be rescaled only after every
       // issued PV (up to s-1) retired (PVs retire in order).
@@ -336,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_ready[s & 1]);
+      if (prof_me) ATTN_PROF(1, s, 3);
     }
 
     // Epilogue: O row / l, l = both groups' partial sums (same reference max).
@@ -405,5 +434,16 @@ void attention_prefill_tc(const AttnCtx& c, const CUtensorMap& kv_map, int work_
   }
   launch_k(attn_tc_kernel, dim3(work_cap, c.nkv), dim3(kThreads), smem, st, kv_map, c);
 }
+
+#ifdef LP_ATTN_PROF
+extern "C" int lp_debug_attn_prof(unsigned long long* out, size_t n) {
+  const size_t bytes = std::min(n * sizeof(unsigned long long), sizeof(g_attn_prof));
+  return cudaMemcpyFromSymbol(out, g_attn_prof, bytes) == cudaSuccess ? 0 : -1;
+}
+extern "C" int lp_debug_attn_prof_reset() {
+  static unsigned long long zero[kProfCtas][3][kProfSteps][4];
+  return cudaMemcpyToSymbol(g_attn_prof, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 }  // namespace lp
