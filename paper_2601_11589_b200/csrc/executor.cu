@@ -76,6 +76,16 @@ constexpr double kTileOverheadCols = 80.0;
 // the last wave is nearly full: time ~ waves * (tile width + kTileOverheadCols)
 // * (K-blocks per split + 2), +3% per extra split (fp32 partial round trip). Tile widths
 // are multiples of 16 (the MMA N is a runtime operand).
+// Relative cost of each extra split-K slice in the tile planner (fp32 partial
+// write + reduce). LP_SPLIT_PENALTY overrides it for experiments.
+static double split_penalty() {
+  static const double v = [] {
+    const char* e = std::getenv("LP_SPLIT_PENALTY");
+    return e ? std::atof(e) : 0.03;
+  }();
+  return v;
+}
+
 TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms) {
   TilePlan t;
   const int base = std::max(1, (n_live + p.bn - 1) / p.bn);
@@ -93,7 +103,7 @@ TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms) {
     for (int s = 1; s <= p.s_cap; ++s) {
       const long units = long(m_tiles) * nt * s;
       const double waves = static_cast<double>((units + workers - 1) / workers);
-      const double cost = waves * (tw + kTileOverheadCols) * (double(nk) / s + 2.0) * (1.0 + 0.03 * (s - 1));
+      const double cost = waves * (tw + kTileOverheadCols) * (double(nk) / s + 2.0) * (1.0 + split_penalty() * (s - 1));
       if (cost < best * (1 - 1e-9)) {
         best = cost;
         t.n_tiles = nt;
