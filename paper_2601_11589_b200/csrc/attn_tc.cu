@@ -84,6 +84,12 @@ __device__ __forceinline__ uint32_t tile_addr(uint32_t base, int r, int c) {
   return base + (c >> 3) * kHalfBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4);
 }
 
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Diagnostic build only (-DLP_ATTN_PROF, scripts/attn_prof.py): clock64
 // stamps per step for the MMA issuer, one softmax warp and the K producer of
 // the first kProfCtas CTAs of KV head 0. Compiled out of the product library.
@@ -317,9 +323,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float corr = grow ? exp2f(m_run - m_use) : 1.f;
       m_run = m_new;
       float sum = 0.f;
+      // ex2.approx.ftz: one MUFU op per element. exp2f adds a range check and
+      // two conditional scalings per element (denormal results), ~3 extra
+      // issue slots each; arguments here are <= kRescaleTau and results below
+      // 2^-126 are negligible against the row sum.
 #pragma unroll
       for (int k = 0; k < kHalf; ++k) {
-        sc[k] = exp2f(sc[k] * c.scale_log2 - m_use);
+        sc[k] = ex2_ftz(sc[k] * c.scale_log2 - m_use);
         sum += sc[k];
       }
       l_run = l_run * corr + sum;
