@@ -190,8 +190,8 @@ __global__ void __launch_bounds__(128)
       float sum = 0.f;
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
-        const float p0 = exp2f(s[nt][2 * hr] * c.scale_log2 - m_use);
-        const float p1 = exp2f(s[nt][2 * hr + 1] * c.scale_log2 - m_use);
+        const float p0 = ex2_ftz(s[nt][2 * hr] * c.scale_log2 - m_use);
+        const float p1 = ex2_ftz(s[nt][2 * hr + 1] * c.scale_log2 - m_use);
         s[nt][2 * hr] = p0;
         s[nt][2 * hr + 1] = p1;
         sum += p0 + p1;

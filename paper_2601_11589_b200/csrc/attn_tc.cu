@@ -84,12 +84,6 @@ __device__ __forceinline__ uint32_t tile_addr(uint32_t base, int r, int c) {
   return base + (c >> 3) * kHalfBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4);
 }
 
-__device__ __forceinline__ float ex2_ftz(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
 // Diagnostic build only (-DLP_ATTN_PROF, scripts/attn_prof.py): clock64
 // stamps per step for the MMA issuer, one softmax warp and the K producer of
 // the first kProfCtas CTAs of KV head 0. Compiled out of the product library.

@@ -1,6 +1,7 @@
-"""A/B timing of a 7B 512-token long-prefill chunk at history H with a given
-build of the native library (experiments: compare two kernel variants on the
-same box back to back). usage: ab_chunk.py LIB_PATH [H] [ITERS]"""
+"""A/B timing of one forward shape with a given build of the native library
+(experiments: compare two kernel variants on the same box back to back).
+usage: ab_chunk.py LIB_PATH chunk H [ITERS]
+       ab_chunk.py LIB_PATH graph L_PAD DEPTH H [ITERS]   (7B, members L ~ U(l_pad/2+1, l_pad))"""
 import sys
 from pathlib import Path
 
@@ -11,21 +12,33 @@ sys.path.insert(0, str(ROOT))
 from paper_2601_11589_b200 import _native as N  # noqa: E402
 
 N.LIB_PATH = Path(sys.argv[1]).resolve()
-from paper_2601_11589_b200.instance import KIND_STANDARD, QWEN25_7B, Member, PrefillInstance  # noqa: E402
+from paper_2601_11589_b200.instance import KIND_GRAPH, KIND_STANDARD, QWEN25_7B, Member, PrefillInstance  # noqa: E402
 
-H = int(sys.argv[2]) if len(sys.argv) > 2 else 3584
-iters = int(sys.argv[3]) if len(sys.argv) > 3 else 7
+mode = sys.argv[2]
 m = QWEN25_7B
-inst = PrefillInstance(m, max_tokens=4096, max_members=8, kv_pages=256)
-inst.capture_graphs(lengths=(16,), depths=(1,))
 rng = np.random.default_rng(0)
-ts = []
+if mode == "chunk":
+    lp, dp, H = 512, 1, int(sys.argv[3])
+    iters = int(sys.argv[4]) if len(sys.argv) > 4 else 7
+else:
+    lp, dp, H = int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
+    iters = int(sys.argv[6]) if len(sys.argv) > 6 else 7
+inst = PrefillInstance(m, max_tokens=max(4096, lp * dp), max_members=max(8, dp), kv_pages=max(256, dp * (H + lp) // 64 + 64))
+inst.capture_graphs(lengths=(lp if mode == "graph" else 16,), depths=(dp if mode == "graph" else 1,))
+ts, sid = [], 10
 for it in range(iters + 2):
-    s = 10 + it
-    if H:
-        inst.forward(H, 1, KIND_STANDARD, [Member(0, s, H, 0)], rng.integers(0, m.vocab, H).astype(np.int32))
-    t = inst.forward(512, 1, KIND_STANDARD, [Member(0, s, 512, H)], rng.integers(0, m.vocab, 512).astype(np.int32))
+    ms = []
+    for i in range(dp):
+        sid += 1
+        for p in range(0, H, 4096):
+            n = min(4096, H - p)
+            inst.forward(n, 1, KIND_STANDARD, [Member(0, sid, n, p)], rng.integers(0, m.vocab, n).astype(np.int32))
+        L = lp if mode == "chunk" else int(rng.integers(lp // 2 + 1, lp + 1))
+        ms.append(Member(i, sid, L, H))
+    toks = rng.integers(0, m.vocab, sum(x.new_tokens for x in ms)).astype(np.int32)
+    t = inst.forward(lp, dp, KIND_STANDARD if mode == "chunk" else KIND_GRAPH, ms, toks)
     if it >= 2:
         ts.append(t)
-    inst.release(s)
-print(f"{N.LIB_PATH.parent.name}: chunk 512 at H={H}: median {np.median(ts):.3f} ms  min {min(ts):.3f}")
+    for x in ms:
+        inst.release(x.session_id)
+print(f"{N.LIB_PATH.parent.name}: {mode} {lp}x{dp} H={H}: median {np.median(ts):.3f} ms  min {min(ts):.3f}")
