@@ -283,3 +283,24 @@ def test_7b_full_depth_against_oracle():
     _compare(inst, oracle, pages, 64, 2, KIND_GRAPH, [M(0, 0, 40, 0), M(1, 1, 24, 0)], check_tokens=False, tol=tol)
     _compare(inst, oracle, pages, 64, 2, KIND_GRAPH, [M(2, 0, 30, 40)], check_tokens=False, tol=tol)
     inst.close()
+
+
+def test_tcgen05_attention_long_history_small_model():
+    """The tcgen05 attention kernel (head_dim 128) over long key ranges on a
+    small model the CPU oracle evaluates in seconds: a 6000-token eager prefill
+    (47 causal 128-key steps for the last row blocks, FMA-pipe exponentials,
+    lazy rescale), a 512-token chunk over that history (chunk graph, key
+    splits merged by the last split CTA) and graph re-prefills on top."""
+    from paper_2601_11589_b200.instance import ModelConfig
+    dims = dict(hidden=512, intermediate=1024, layers=2, n_q_heads=4, n_kv_heads=1, head_dim=128, vocab=1024)
+    inst = PrefillInstance(ModelConfig(**dims), max_tokens=8192, max_members=8, kv_pages=512)
+    inst.capture_graphs(lengths=(16, 64), depths=(1, 4))
+    oracle = FO.OracleModel(FO.ModelSpec(**dims))
+    pages = PageOracle(512)
+    _compare(inst, oracle, pages, 0, 0, KIND_PACKED, [Member(0, 1, 6000, 0)])
+    _compare(inst, oracle, pages, 512, 1, KIND_STANDARD, [Member(0, 1, 512, 6000)])
+    _compare(inst, oracle, pages, 64, 4, KIND_GRAPH,
+             [Member(0, 1, 40, 6512), Member(1, 2, 64, 0), Member(2, 3, 17, 0)])
+    _compare(inst, oracle, pages, 16, 1, KIND_GRAPH, [Member(0, 1, 9, 6552)])
+    _kv_check(inst, oracle, 1, [0, 1])
+    inst.close()
