@@ -1,7 +1,7 @@
 """A/B timing of one forward shape with a given build of the native library
 (experiments: compare two kernel variants on the same box back to back).
 usage: ab_chunk.py LIB_PATH chunk H [ITERS]
-       ab_chunk.py LIB_PATH graph L_PAD DEPTH H [ITERS]   (7B, members L ~ U(l_pad/2+1, l_pad))"""
+       ab_chunk.py LIB_PATH graph L_PAD DEPTH H [ITERS]   (AB_MODEL, default qwen2.5-7b; members L ~ U(l_pad/2+1, l_pad))"""
 import sys
 from pathlib import Path
 
@@ -12,10 +12,11 @@ sys.path.insert(0, str(ROOT))
 from paper_2601_11589_b200 import _native as N  # noqa: E402
 
 N.LIB_PATH = Path(sys.argv[1]).resolve()
-from paper_2601_11589_b200.instance import KIND_GRAPH, KIND_STANDARD, QWEN25_7B, Member, PrefillInstance  # noqa: E402
+from paper_2601_11589_b200.instance import KIND_GRAPH, KIND_STANDARD, MODELS, Member, PrefillInstance  # noqa: E402
 
 mode = sys.argv[2]
-m = QWEN25_7B
+import os
+m = MODELS[os.environ.get("AB_MODEL", "qwen2.5-7b")]
 rng = np.random.default_rng(0)
 if mode == "chunk":
     lp, dp, H = 512, 1, int(sys.argv[3])
