@@ -71,7 +71,7 @@ typedef struct lp_model_desc {
 
 typedef struct lp_instance_desc {
   int32_t device;
-  int32_t page_size;     /* tokens per KV page (power of two, 16..128) */
+  int32_t page_size;     /* tokens per KV page: 0 (default) or 64 — the attention key tile */
   int64_t kv_pages;      /* pool size in pages; 0 = size from free HBM */
   int64_t max_tokens;    /* activation arena capacity (tokens per forward) */
   int32_t max_members;   /* max requests per forward */

@@ -1,0 +1,47 @@
+/*
+ * laps_prefill_testing.h — kernel-level test hooks of liblaps_prefill.so.
+ *
+ * NOT part of the drop-in boundary (that is laps_prefill.h). These entry
+ * points let the parity tests and the measurement scripts drive single
+ * sm_100a kernels on raw device pointers or time one projection inside an
+ * instance. Same conventions as laps_prefill.h: int status, LP_ERR_* codes,
+ * lp_last_error() for the text, no exceptions across the boundary.
+ */
+#ifndef LAPS_PREFILL_TESTING_H_
+#define LAPS_PREFILL_TESTING_H_
+
+#include <stdint.h>
+
+#include "laps_prefill.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Epilogue modes of lpk_gemm (csrc/gemm_sm100.cuh kEpi*). */
+#define LPK_EPI_BF16 0        /* out_bf16[n*ldo + m] = acc (+ bias[m]) */
+#define LPK_EPI_F32_PARTIAL 1 /* fp32 split-K partials ws[(split*N + n)*M + m] */
+#define LPK_EPI_SILU_MUL 2    /* row-interleaved gate/up -> bf16 SiLU(gate)*up */
+#define LPK_EPI_F32 3         /* out_f32[n*ldo + m] = acc */
+
+/* One tcgen05 GEMM launch: out[N, M] = X[N, K] . W[M, K]^T on `stream`
+ * (cudaStream_t), device pointers only. bn = token tile (16..256), pair = 1
+ * or 2 (cta_group::2), n_dev = device int holding the live token count. */
+int lpk_gemm(const void* W, const void* X, void* out, float* ws, const void* bias, int M, int N, int K,
+             int splits, int mode, int bn, int ldo, const int* n_dev, void* stream, int pair);
+
+/* Time one projection of layer `layer` inside an instance (which: 0 QKV,
+ * 1 O, 2 gate/up + SiLU, 3 down) at capacity t_cap with n_live live tokens:
+ * *avg_ms = mean CUDA-event time over `iters` back-to-back launches. */
+int lpk_time_gemm(lp_instance* inst, int32_t layer, int32_t which, int32_t t_cap, int32_t n_live,
+                  int32_t iters, double* avg_ms);
+
+/* bf16 bits of weight element `index` of tensor `tensor_id` from the device
+ * initialiser's generator (host side; the oracle must reproduce them). */
+uint16_t lpk_synth_weight_bits(uint64_t seed, uint64_t tensor_id, uint64_t index, float scale);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LAPS_PREFILL_TESTING_H_ */

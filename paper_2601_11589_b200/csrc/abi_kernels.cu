@@ -1,4 +1,4 @@
-// Kernel-level C-ABI test hooks (include/laps_prefill_testing.h). These let
+// Kernel-level C-ABI test hooks (declared in include/laps_prefill_testing.h). These let
 // the parity tests drive each sm_100a kernel on raw device pointers without
 // going through a full instance. Product callers use include/laps_prefill.h.
 #include <cstdio>

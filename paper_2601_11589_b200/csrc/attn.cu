@@ -281,11 +281,7 @@ template <int D>
 void launch(const AttnCtx& c, const CUtensorMap& kvm, int work_cap, int combine_cap, bool with_combine,
             cudaStream_t st) {
   constexpr int smem = 1024 + 5 * 64 * D * 2 + 64;
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(attn_prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    set = true;
-  }
+  smem_attr_once(reinterpret_cast<const void*>(attn_prefill_kernel<D>), smem);
   launch_k(attn_prefill_kernel<D>, dim3(work_cap, c.nkv), dim3(128), smem, st, kvm, c);
   // Graph-bucket shapes split long histories into many short key ranges
   // (up to 32 per 64-row block): a separate merge grid (one warp per row,

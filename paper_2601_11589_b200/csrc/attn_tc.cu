@@ -3,7 +3,7 @@
 // ... and for long-prompt attention").
 //
 // One CTA = 128 packed (token, q-head) rows of one KV group x a key range.
-// Roles (192 threads):
+// Roles (320 threads = 10 warps, kThreads):
 //   warp 0   TMA producers (lane 0 K, lane 1 V): pages (2 pages = 128 keys
 //            per step) into separate 3-stage K and V rings, laid out
 //            [d-half][128 keys][128 B] (128B swizzle);
@@ -446,11 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 void attention_prefill_tc(const AttnCtx& c, const CUtensorMap& kv_map, int work_cap, cudaStream_t st) {
   constexpr int smem = TcSmem::kTotal;
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    set = true;
-  }
+  smem_attr_once(reinterpret_cast<const void*>(attn_tc_kernel), smem);
   launch_k(attn_tc_kernel, dim3(work_cap, c.nkv), dim3(kThreads), smem, st, kv_map, c);
 }
 

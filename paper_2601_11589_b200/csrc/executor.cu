@@ -934,6 +934,15 @@ struct lp_instance {
   Instance* impl;
 };
 
+namespace {
+// Every entry point that takes a handle validates it: a null handle is an
+// LP_ERR_CONFIG status, never a crash.
+Instance& impl_of(lp_instance* inst) {
+  if (!inst || !inst->impl) throw lp::ConfigError("null instance handle");
+  return *inst->impl;
+}
+}  // namespace
+
 extern "C" {
 
 int lp_instance_create(const lp_model_desc* model, const lp_instance_desc* desc, lp_instance** out) {
@@ -962,15 +971,16 @@ int lp_instance_destroy(lp_instance* inst) {
 int lp_instance_model(lp_instance* inst, lp_model_desc* out) {
   return lp::lp_guard([&] {
     if (!inst || !out) throw lp::ConfigError("null argument");
-    *out = inst->impl->model();
+    *out = impl_of(inst).model();
   });
 }
 
 int lp_capture_graphs(lp_instance* inst, const int64_t* lengths, int32_t n_lengths, const int32_t* depths,
                       int32_t n_depths) {
   return lp::lp_guard([&] {
-    if (!inst) throw lp::ConfigError("null instance");
-    inst->impl->capture_graphs(std::vector<int64_t>(lengths, lengths + n_lengths),
+    if (n_lengths > 0 && !lengths) throw lp::ConfigError("null argument");
+    if (n_depths > 0 && !depths) throw lp::ConfigError("null argument");
+    impl_of(inst).capture_graphs(std::vector<int64_t>(lengths, lengths + n_lengths),
                                std::vector<int32_t>(depths, depths + n_depths));
   });
 }
@@ -978,69 +988,88 @@ int lp_capture_graphs(lp_instance* inst, const int64_t* lengths, int32_t n_lengt
 int lp_submit(lp_instance* inst, const lp_shape* shape, const lp_member* members, int32_t n,
               const int32_t* token_ids) {
   return lp::lp_guard([&] {
-    if (!inst || !shape || !members || !token_ids) throw lp::ConfigError("null argument");
-    inst->impl->submit(*shape, members, n, token_ids);
+    if (!shape || !members || !token_ids) throw lp::ConfigError("null argument");
+    impl_of(inst).submit(*shape, members, n, token_ids);
   });
 }
 
 int lp_last_io(lp_instance* inst, int64_t* h2d_bytes, int64_t* d2h_bytes) {
   return lp::lp_guard([&] {
-    if (h2d_bytes) *h2d_bytes = static_cast<int64_t>(inst->impl->last_h2d_bytes_);
-    if (d2h_bytes) *d2h_bytes = static_cast<int64_t>(inst->impl->last_d2h_bytes_);
+    if (h2d_bytes) *h2d_bytes = static_cast<int64_t>(impl_of(inst).last_h2d_bytes_);
+    if (d2h_bytes) *d2h_bytes = static_cast<int64_t>(impl_of(inst).last_d2h_bytes_);
   });
 }
 
 int lp_last_launches(lp_instance* inst, int32_t* kernels) {
   return lp::lp_guard([&] {
-    if (kernels) *kernels = inst->impl->last_launches_;
+    if (kernels) *kernels = impl_of(inst).last_launches_;
   });
 }
 
 int lp_timer_record(lp_instance* inst, int32_t slot) {
-  return lp::lp_guard([&] { inst->impl->timer_record(slot); });
+  return lp::lp_guard([&] { impl_of(inst).timer_record(slot); });
 }
 
 int lp_timer_elapsed(lp_instance* inst, int32_t slot_a, int32_t slot_b, double* ms) {
-  return lp::lp_guard([&] { *ms = inst->impl->timer_elapsed(slot_a, slot_b); });
+  return lp::lp_guard([&] {
+    if (!ms) throw lp::ConfigError("null argument");
+    *ms = impl_of(inst).timer_elapsed(slot_a, slot_b);
+  });
 }
 
 int lpk_time_gemm(lp_instance* inst, int32_t layer, int32_t which, int32_t t_cap, int32_t n_live,
                   int32_t iters, double* avg_ms) {
-  return lp::lp_guard([&] { *avg_ms = inst->impl->time_gemm(layer, which, t_cap, n_live, iters); });
+  return lp::lp_guard([&] {
+    if (!avg_ms) throw lp::ConfigError("null argument");
+    *avg_ms = impl_of(inst).time_gemm(layer, which, t_cap, n_live, iters);
+  });
 }
 
 int lp_wait(lp_instance* inst, double* service_ms) {
   return lp::lp_guard([&] {
-    if (!inst) throw lp::ConfigError("null instance");
-    const double ms = inst->impl->wait();
+    const double ms = impl_of(inst).wait();
     if (service_ms) *service_ms = ms;
   });
 }
 
 int lp_read_next_tokens(lp_instance* inst, int32_t* out, int32_t n) {
-  return lp::lp_guard([&] { inst->impl->read_next_tokens(out, n); });
+  return lp::lp_guard([&] {
+    if (!out && n > 0) throw lp::ConfigError("null argument");
+    impl_of(inst).read_next_tokens(out, n);
+  });
 }
 
 int lp_read_logits(lp_instance* inst, float* out, size_t cap_floats) {
-  return lp::lp_guard([&] { inst->impl->read_logits(out, cap_floats); });
+  return lp::lp_guard([&] {
+    if (!out) throw lp::ConfigError("null argument");
+    impl_of(inst).read_logits(out, cap_floats);
+  });
 }
 
 int lp_session_pages(lp_instance* inst, int64_t session_id, int32_t* pages, int32_t cap, int32_t* n_pages,
                      int64_t* kv_len) {
-  return lp::lp_guard([&] { inst->impl->session_pages(session_id, pages, cap, n_pages, kv_len); });
+  return lp::lp_guard([&] { impl_of(inst).session_pages(session_id, pages, cap, n_pages, kv_len); });
 }
 
 int lp_session_release(lp_instance* inst, int64_t session_id) {
-  return lp::lp_guard([&] { inst->impl->session_release(session_id); });
+  return lp::lp_guard([&] { impl_of(inst).session_release(session_id); });
 }
 
 int lp_read_kv(lp_instance* inst, int64_t session_id, int32_t layer, int64_t pos0, int64_t n, uint16_t* k_out,
                uint16_t* v_out) {
-  return lp::lp_guard([&] { inst->impl->read_kv(session_id, layer, pos0, n, k_out, v_out); });
+  return lp::lp_guard([&] {
+    if (!k_out || !v_out) throw lp::ConfigError("null argument");
+    impl_of(inst).read_kv(session_id, layer, pos0, n, k_out, v_out);
+  });
 }
 
 int lp_session_migrate(lp_instance* src, lp_instance* dst, int64_t session_id) {
-  return lp::lp_guard([&] { Instance::migrate(*src->impl, *dst->impl, session_id); });
+  return lp::lp_guard([&] {
+    Instance& a = impl_of(src);
+    Instance& b = impl_of(dst);
+    if (&a == &b) throw lp::ConfigError("lp_session_migrate: source and destination are the same instance");
+    Instance::migrate(a, b, session_id);
+  });
 }
 
 }  // extern "C"

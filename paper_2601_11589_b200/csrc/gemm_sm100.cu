@@ -8,6 +8,7 @@
 //               so every activation byte crosses L2->SM once per 256 weight
 //               rows (not per 128) and per-SM shared-memory operand traffic
 //               halves. Used for token tiles of >= 128 columns.
+#include <atomic>
 #include <algorithm>
 #include <cstdio>
 #include <mutex>
@@ -405,12 +406,8 @@ template <int BN, int kPair>
 void launch_bn(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                cudaStream_t stream, int max_ctas) {
   using C = Cfg<BN, kPair>;
-  static bool attr_set = false;
   auto* kern = gemm_bf16_tn_kernel<BN, kPair>;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    attr_set = true;
-  }
+  smem_attr_once(reinterpret_cast<const void*>(kern), C::kSmem);
   const int units = a.splits * (a.M / (kBM * kPair)) * std::max((a.N + BN - 1) / BN, a.n_tiles_cap);
   int grid = num_sms() / kPair;
   if (max_ctas > 0 && max_ctas / kPair < grid) grid = max_ctas / kPair;
@@ -440,12 +437,16 @@ void launch_bn(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a
 }  // namespace
 
 int num_sms() {
-  static int n = 0;
+  // Per device: a process may drive several GPUs (one instance each).
+  static std::atomic<int> cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& slot = cache[dev & 63];
+  int n = slot.load(std::memory_order_relaxed);
   if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    slot.store(n, std::memory_order_relaxed);
   }
   return n;
 }

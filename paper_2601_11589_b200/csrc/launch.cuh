@@ -14,6 +14,11 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <utility>
 
 namespace lp {
 
@@ -53,5 +58,22 @@ inline bool debug_empty(const char* cls) {
   return e && std::strstr(e, cls) != nullptr;
 }
 void launch_empty(dim3 grid, dim3 block, cudaStream_t st);
+
+// Raise a kernel's dynamic shared-memory limit on the CURRENT device, once
+// per (kernel, device). The attribute lives in the device's context, so a
+// process driving several GPUs (one instance per device, possibly from
+// different host threads) must set it on every device it launches on.
+inline void smem_attr_once(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({kernel, dev})) return;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string("cudaFuncSetAttribute(max dynamic smem): ") + cudaGetErrorString(e));
+  done.insert({kernel, dev});
+}
 
 }  // namespace lp

@@ -16,10 +16,10 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def _declared(header: Path) -> list[str]:
     text = header.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|int32_t|const char\*|uint16_t)\s+(lp_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|const char\*|uint16_t)\s+(lpk?_\w+)\s*\(", text, re.M)))
 
 
-@pytest.mark.parametrize("header", ["laps_prefill.h", "laps_engine.h"])
+@pytest.mark.parametrize("header", ["laps_prefill.h", "laps_engine.h", "laps_prefill_testing.h"])
 def test_every_declared_symbol_is_exported(header):
     lib = N.lib()
     names = _declared(ROOT / "include" / header)
