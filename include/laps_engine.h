@@ -12,10 +12,18 @@
  *                      reference's for the same config.
  *   LP_SIM_REPLAY      as above for the clock (so batch composition, queue
  *                      assignment, padding and chunking stay byte-identical),
- *                      and every dispatch ALSO executes on its GPU instance;
- *                      measured forward times are reported alongside.
- *   LP_SIM_LIVE        the clock advances by the measured GPU service time:
- *                      real TTFT / req/s of the B200 path under the policy.
+ *                      and every dispatch ALSO executes on its GPU instance.
+ *                      The engine does not wait for the GPU: forwards of
+ *                      different instances run concurrently, measured times
+ *                      are collected as they finish.
+ *   LP_SIM_LIVE        virtual clock advanced by the measured GPU service time
+ *                      of each forward (waits for every forward).
+ *   LP_SIM_WALL        wall clock (steady_clock): arrivals are released in real
+ *                      time, completions are the GPU's CUDA events, the
+ *                      instances serve concurrently; TTFT includes engine,
+ *                      H2D, launch and D2H time. With no instances the
+ *                      forwards are emulated by sleeping for the cost-model
+ *                      service time (host-side tests of the wall clock).
  */
 #ifndef LAPS_ENGINE_H_
 #define LAPS_ENGINE_H_
@@ -31,6 +39,7 @@ extern "C" {
 #define LP_SIM_COST_MODEL 0
 #define LP_SIM_REPLAY 1
 #define LP_SIM_LIVE 2
+#define LP_SIM_WALL 3
 
 typedef struct lp_sim_stats {
   int64_t arrivals;
@@ -46,7 +55,28 @@ typedef struct lp_sim_stats {
   double slo_violation;
   double gpu_ms_total;       /* sum of measured forward times */
   double engine_wall_s;      /* host wall time of the whole run */
+  /* Timed window (lp_sim_opts); zero when no window was requested. */
+  int64_t window_dispatches;  /* engine dispatches executed inside the window */
+  int64_t window_requests;    /* requests whose final forward is in the window */
+  int64_t window_fills;       /* history-fill forwards inside the window */
+  int64_t window_kernels;     /* kernels the window's forwards launched */
+  int64_t window_h2d_bytes;   /* token ids + metadata copied host->device */
+  int64_t window_d2h_bytes;   /* first tokens copied device->host */
+  double window_device_ms;    /* max over instances: CUDA-event time from
+                                 before the window's first forward to after
+                                 its last one, on each instance's stream */
+  double window_wall_ms;      /* host steady_clock from the first window
+                                 submit until every window forward finished
+                                 and its first tokens were read on the host */
 } lp_sim_stats;
+
+/* Run options (all zero = lp_sim_run). */
+typedef struct lp_sim_opts {
+  int64_t window_first;  /* GPU dispatches [first, first + count) form the  */
+  int64_t window_count;  /* timed window (REPLAY mode); 0 = no window      */
+  int32_t stop_after_window;  /* 1: later dispatches run on the clock only  */
+  int32_t reserved;
+} lp_sim_opts;
 
 /* Run a scenario. cfg_text / overrides: `key = value` lines (reference key
  * names). out_dir: if non-empty, events.log + metrics.json (+ forwards.csv
@@ -55,6 +85,11 @@ typedef struct lp_sim_stats {
  * token_seed: seed of the synthetic token ids (lp_synth_token). */
 int lp_sim_run(const char* cfg_text, const char* overrides, const char* out_dir, int32_t mode,
                lp_instance** insts, int32_t n_insts, uint64_t token_seed, lp_sim_stats* stats);
+
+/* lp_sim_run with options (a timed window of dispatches for benchmarks). */
+int lp_sim_run_ex(const char* cfg_text, const char* overrides, const char* out_dir, int32_t mode,
+                  lp_instance** insts, int32_t n_insts, uint64_t token_seed, const lp_sim_opts* opts,
+                  lp_sim_stats* stats);
 
 /* The reference CLI's `prefillsim sweep --param P --values v1,v2,...`
  * (tools/main.cpp:114-168): for each value (sorted ascending) apply

@@ -124,6 +124,23 @@ int lp_submit(lp_instance* inst, const lp_shape* shape, const lp_member* members
 /* Block until the last submit finished; *service_ms = device time of the
  * forward (CUDA events on the instance stream). */
 int lp_wait(lp_instance* inst, double* service_ms);
+/* Ticketed form of lp_submit for pipelined / multi-instance drivers: the
+ * forward is queued on the instance's stream and *ticket identifies it.
+ * Metadata for up to 4 forwards can be staged ahead of the GPU; results (the
+ * device time and the greedy first tokens, copied to pinned host memory at
+ * the end of the forward) stay readable for the last 16 submits of the
+ * instance — an older ticket is LP_ERR_STATE. lp_submit == lp_submit_async
+ * with the ticket kept as "the last submit". */
+int lp_submit_async(lp_instance* inst, const lp_shape* shape, const lp_member* members, int32_t n,
+                    const int32_t* token_ids, int64_t* ticket);
+/* *done = 1 once the forward and its first-token copy finished (cudaEventQuery;
+ * never blocks). */
+int lp_ticket_query(lp_instance* inst, int64_t ticket, int32_t* done);
+/* Block until the ticket's forward finished; *service_ms = its device time. */
+int lp_ticket_wait(lp_instance* inst, int64_t ticket, double* service_ms);
+/* Greedy first tokens of the ticket's members (blocks until available). */
+int lp_ticket_tokens(lp_instance* inst, int64_t ticket, int32_t* out, int32_t n);
+
 /* Greedy first token (argmax of the last real token's logits) per member of
  * the last submit, in member order. */
 int lp_read_next_tokens(lp_instance* inst, int32_t* out, int32_t n);
@@ -131,7 +148,8 @@ int lp_read_next_tokens(lp_instance* inst, int32_t* out, int32_t n);
 int lp_read_logits(lp_instance* inst, float* out, size_t cap_floats);
 
 /* Host->device bytes copied by the last lp_submit (token ids + metadata)
- * and device->host bytes of the last lp_read_next_tokens. */
+ * and device->host bytes of its result (the first tokens, copied at the end
+ * of every forward). */
 int lp_last_io(lp_instance* inst, int64_t* h2d_bytes, int64_t* d2h_bytes);
 /* Kernels the last lp_submit put on the GPU (graph kernel nodes or eager
  * launches): 1 + layers x (8 or 9) + 3. */
@@ -151,9 +169,15 @@ int lp_session_release(lp_instance* inst, int64_t session_id);
  * [pos0, pos0+n) of one layer to host buffers. */
 int lp_read_kv(lp_instance* inst, int64_t session_id, int32_t layer, int64_t pos0, int64_t n,
                uint16_t* k_out, uint16_t* v_out);
-/* Export / import a session's KV to another instance (P2P over NVLink when
- * the devices differ). */
+/* Move a session's KV to another instance (P2P over NVLink when the devices
+ * differ). Asynchronous: the copy is ordered after the source's queued
+ * forwards (event) and before the destination's next ones (its stream), and
+ * the source's later work waits for the copy before reusing the pages. */
 int lp_session_migrate(lp_instance* src, lp_instance* dst, int64_t session_id);
+/* As lp_session_migrate, but the source keeps its copy (a session whose
+ * long-prompt chunks are still running there while a later turn is served
+ * elsewhere). */
+int lp_session_copy(lp_instance* src, lp_instance* dst, int64_t session_id);
 
 /* ---- deterministic synthetic inputs (shared with the CPU oracle) ---- */
 /* token id of (seed, session, position): splitmix64 mix mod vocab. */

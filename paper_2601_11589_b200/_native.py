@@ -76,8 +76,9 @@ PUBLIC_SYMBOLS = [
     "lp_read_next_tokens", "lp_read_logits", "lp_session_pages", "lp_session_release",
     "lp_read_kv", "lp_session_migrate", "lp_synth_token", "lp_last_error", "lp_version",
     "lp_instance_model", "lp_timer_record", "lp_timer_elapsed", "lp_last_io", "lp_last_launches",
+    "lp_submit_async", "lp_ticket_query", "lp_ticket_wait", "lp_ticket_tokens", "lp_session_copy",
 ]
-ENGINE_SYMBOLS = ["lp_sim_run", "lp_sim_trace", "lp_sim_sweep"]  # include/laps_engine.h
+ENGINE_SYMBOLS = ["lp_sim_run", "lp_sim_run_ex", "lp_sim_trace", "lp_sim_sweep"]  # include/laps_engine.h
 
 
 def _declare(L: ctypes.CDLL) -> None:
@@ -97,6 +98,11 @@ def _declare(L: ctypes.CDLL) -> None:
     sig("lp_submit", c_i32, vp, ctypes.POINTER(Shape), ctypes.POINTER(Member), c_i32,
         ctypes.POINTER(c_i32))
     sig("lp_wait", c_i32, vp, ctypes.POINTER(c_f64))
+    sig("lp_submit_async", c_i32, vp, ctypes.POINTER(Shape), ctypes.POINTER(Member), c_i32,
+        ctypes.POINTER(c_i32), ctypes.POINTER(c_i64))
+    sig("lp_ticket_query", c_i32, vp, c_i64, ctypes.POINTER(c_i32))
+    sig("lp_ticket_wait", c_i32, vp, c_i64, ctypes.POINTER(c_f64))
+    sig("lp_ticket_tokens", c_i32, vp, c_i64, ctypes.POINTER(c_i32), c_i32)
     sig("lp_read_next_tokens", c_i32, vp, ctypes.POINTER(c_i32), c_i32)
     sig("lp_read_logits", c_i32, vp, ctypes.POINTER(c_f32), ctypes.c_size_t)
     sig("lp_session_pages", c_i32, vp, c_i64, ctypes.POINTER(c_i32), c_i32, ctypes.POINTER(c_i32),
@@ -104,6 +110,7 @@ def _declare(L: ctypes.CDLL) -> None:
     sig("lp_session_release", c_i32, vp, c_i64)
     sig("lp_read_kv", c_i32, vp, c_i64, c_i32, c_i64, c_i64, vp, vp)
     sig("lp_session_migrate", c_i32, vp, vp, c_i64)
+    sig("lp_session_copy", c_i32, vp, vp, c_i64)
     sig("lp_instance_model", c_i32, vp, ctypes.POINTER(ModelDesc))
     sig("lp_timer_record", c_i32, vp, c_i32)
     sig("lp_last_io", c_i32, vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64))

@@ -23,6 +23,9 @@ struct OutOfMemory : std::runtime_error {
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct StateError : std::runtime_error {  // call out of order / expired ticket
+  using std::runtime_error::runtime_error;
+};
 
 void set_last_error(const std::string& msg);
 
@@ -49,6 +52,9 @@ int lp_guard(F&& f) {
   } catch (const CudaError& e) {
     set_last_error(e.what());
     return LP_ERR_CUDA;
+  } catch (const StateError& e) {
+    set_last_error(e.what());
+    return LP_ERR_STATE;
   } catch (const std::exception& e) {
     set_last_error(e.what());
     return LP_ERR_INTERNAL;

@@ -157,8 +157,14 @@ Instance::Instance(const lp_model_desc& m, const lp_instance_desc& d) : m_(m), d
   lp_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   lp_check(cudaEventCreate(&ev_start_), "event");
   lp_check(cudaEventCreate(&ev_end_), "event");
-  lp_check(cudaEventCreateWithFlags(&ev_h2d_, cudaEventDisableTiming), "event");
   lp_check(cudaEventCreateWithFlags(&ev_mig_, cudaEventDisableTiming), "event");
+  lp_check(cudaEventCreateWithFlags(&ev_mig_done_, cudaEventDisableTiming), "event");
+  for (Staging& sg : staging_) lp_check(cudaEventCreateWithFlags(&sg.h2d, cudaEventDisableTiming), "event");
+  for (Ticket& tk : tickets_) {
+    lp_check(cudaEventCreate(&tk.start), "event");
+    lp_check(cudaEventCreate(&tk.end), "event");
+    lp_check(cudaEventCreateWithFlags(&tk.done, cudaEventDisableTiming), "event");
+  }
   alloc_weights();
   alloc_arena();
 }
@@ -171,12 +177,21 @@ Instance::~Instance() {
   for (auto& [k, g] : graphs_tc_) cudaGraphExecDestroy(g);
   for (auto& [k, g] : chunk_graphs_) cudaGraphExecDestroy(g);
   for (void* p : allocs_) cudaFree(p);
-  if (meta_host_) cudaFreeHost(meta_host_);
   if (mig_host_) cudaFreeHost(mig_host_);
+  for (Staging& sg : staging_) {
+    if (sg.host) cudaFreeHost(sg.host);
+    cudaEventDestroy(sg.h2d);
+  }
+  for (Ticket& tk : tickets_) {
+    if (tk.keys) cudaFreeHost(tk.keys);
+    cudaEventDestroy(tk.start);
+    cudaEventDestroy(tk.end);
+    cudaEventDestroy(tk.done);
+  }
   cudaEventDestroy(ev_start_);
   cudaEventDestroy(ev_end_);
-  cudaEventDestroy(ev_h2d_);
   cudaEventDestroy(ev_mig_);
+  cudaEventDestroy(ev_mig_done_);
   for (cudaEvent_t e : timers_)
     if (e) cudaEventDestroy(e);
   cudaStreamDestroy(stream_);
@@ -304,8 +319,6 @@ void Instance::alloc_arena() {
                o_cb = carve(size_t(c_max_) * 16);
   meta_bytes_ = off;
   meta_dev_ = dmalloc<uint8_t>(meta_bytes_, allocs_);
-  lp_check(cudaMallocHost(&meta_host_, meta_bytes_), "pinned meta");
-  std::memset(meta_host_, 0, meta_bytes_);
   auto bind = [&](void* base, Meta& m) {
     uint8_t* b = static_cast<uint8_t*>(base);
     m.scalars = reinterpret_cast<int*>(b + o_sc);
@@ -322,7 +335,15 @@ void Instance::alloc_arena() {
     m.combine = reinterpret_cast<int4*>(b + o_cb);
   };
   bind(meta_dev_, md_);
-  bind(meta_host_, mh_);
+  for (Staging& sg : staging_) {
+    lp_check(cudaMallocHost(&sg.host, meta_bytes_), "pinned meta");
+    std::memset(sg.host, 0, meta_bytes_);
+    bind(sg.host, sg.m);
+  }
+  mh_ = staging_[0].m;
+  for (Ticket& tk : tickets_)
+    lp_check(cudaMallocHost(reinterpret_cast<void**>(&tk.keys), size_t(r_max_) * sizeof(unsigned long long)),
+             "pinned first tokens");
   lp_check(cudaMemsetAsync(meta_dev_, 0, meta_bytes_, stream_), "meta zero");
   lp_check(cudaStreamSynchronize(stream_), "arena sync");
 }
@@ -490,8 +511,10 @@ void Instance::capture_graphs(const std::vector<int64_t>& lens, const std::vecto
   if (!d_.use_graphs) return;
   lp_check(cudaSetDevice(d_.device), "set device");
   // Warm the launch paths (function attributes, tensor-map cache) eagerly.
-  mh_.scalars[0] = mh_.scalars[1] = mh_.scalars[2] = mh_.scalars[3] = 0;
-  lp_check(cudaMemcpyAsync(md_.scalars, mh_.scalars, 16, cudaMemcpyHostToDevice, stream_), "meta");
+  Meta& mh = acquire_staging();
+  mh.scalars[0] = mh.scalars[1] = mh.scalars[2] = mh.scalars[3] = 0;
+  lp_check(cudaMemcpyAsync(md_.scalars, mh.scalars, 16, cudaMemcpyHostToDevice, stream_), "meta");
+  lp_check(cudaEventRecord(staging_[(stage_seq_ - 1) % kStaging].h2d, stream_), "event");
   for (int64_t L : lens) {
     for (int32_t dep : depths) {
       const int64_t t_cap = L * dep;
@@ -520,11 +543,47 @@ cudaGraphExec_t Instance::capture_one(int t_cap, int r_cap, bool graph_attn, boo
   return exec;
 }
 
-void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const int32_t* tokens) {
+Meta& Instance::acquire_staging() {
+  Staging& sg = staging_[stage_seq_ % kStaging];
+  ++stage_seq_;
+  if (sg.used) lp_check(cudaEventSynchronize(sg.h2d), "staging reuse");
+  sg.used = true;
+  mh_ = sg.m;
+  return mh_;
+}
+
+Instance::Ticket& Instance::ticket(int64_t id) {
+  Ticket& tk = tickets_[((id % kTickets) + kTickets) % kTickets];
+  if (id < 0 || tk.id != id)
+    throw StateError("ticket " + std::to_string(id) + " unknown or expired (results are kept for the last " +
+                     std::to_string(kTickets) + " submits)");
+  return tk;
+}
+
+bool Instance::ticket_done(int64_t id) {
+  const cudaError_t e = cudaEventQuery(ticket(id).done);
+  if (e == cudaErrorNotReady) return false;
+  lp_check(e, "ticket query");
+  return true;
+}
+
+double Instance::ticket_wait(int64_t id) {
+  Ticket& tk = ticket(id);
+  lp_check(cudaEventSynchronize(tk.done), "forward");
+  float ms = 0;
+  lp_check(cudaEventElapsedTime(&ms, tk.start, tk.end), "elapsed");
+  return ms;
+}
+
+void Instance::ticket_tokens(int64_t id, int32_t* out, int n) {
+  Ticket& tk = ticket(id);
+  if (n > tk.n) throw ShapeMismatch("asked for more tokens than members");
+  lp_check(cudaEventSynchronize(tk.done), "first tokens");
+  for (int i = 0; i < n; ++i) out[i] = argmax_token(tk.keys[i]);
+}
+
+int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const int32_t* tokens) {
   lp_check(cudaSetDevice(d_.device), "set device");
-  // The pinned staging block is reused: the previous forward's H2D copies
-  // must have drained before it is rewritten.
-  if (submitted_) lp_check(cudaEventSynchronize(ev_h2d_), "staging reuse");
   if (n < 1) throw ShapeMismatch("empty batch");
   if (n > r_max_) throw ShapeMismatch("batch of " + std::to_string(n) + " exceeds max_members");
   if (shape.kind != LP_KIND_PACKED && n > shape.depth)
@@ -551,7 +610,14 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
     ensure_capacity(s, mem[i].history + mem[i].new_tokens);
   }
 
-  // Host metadata.
+  // Results slot of this forward: the ticket kTickets submits ago is dropped
+  // (its D2H must have landed before the pinned slot is rewritten).
+  const int64_t id = next_ticket_;
+  Ticket& tk = tickets_[id % kTickets];
+  if (tk.id >= 0) lp_check(cudaEventSynchronize(tk.done), "ticket reuse");
+  tk.id = -1;
+  // Host metadata, in the next free pinned staging block.
+  acquire_staging();
   const int G = m_.n_q_heads / m_.n_kv_heads;
   int t = 0, np = 0;
   for (int i = 0; i < n; ++i) {
@@ -698,8 +764,8 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
   h2d(md_.work, mh_.work, size_t(nw) * 16);
   h2d(md_.combine, mh_.combine, size_t(nc) * 16);
 
-  lp_check(cudaEventRecord(ev_h2d_, stream_), "event");
-  lp_check(cudaEventRecord(ev_start_, stream_), "event");
+  lp_check(cudaEventRecord(staging_[(stage_seq_ - 1) % kStaging].h2d, stream_), "event");
+  lp_check(cudaEventRecord(tk.start, stream_), "event");
   if (exec && nc == 0 && shape.kind == LP_KIND_GRAPH && !tc_graph) {
     auto it = graphs_nc_.find(graph_key(shape.l_pad, shape.depth));
     if (it != graphs_nc_.end()) exec = it->second;  // no split: skip the merge grid
@@ -718,13 +784,22 @@ void Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const 
     enqueue_forward(t_cap, r_cap, stream_, false, nc > 0);
   }
   lp_check(cudaGetLastError(), "forward launch");
-  lp_check(cudaEventRecord(ev_end_, stream_), "event");
+  lp_check(cudaEventRecord(tk.end, stream_), "event");
+  // The step's result (greedy first token per member) lands in the ticket's
+  // pinned slot; the host reads it once `done` fires.
+  lp_check(cudaMemcpyAsync(tk.keys, next_keys_, size_t(n) * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           stream_), "first tokens d2h");
+  lp_check(cudaEventRecord(tk.done, stream_), "event");
+  last_d2h_bytes_ = size_t(n) * sizeof(unsigned long long);
+  tk.id = id;
+  tk.n = n;
+  ++next_ticket_;
   for (int i = 0; i < n; ++i) {
     Session& s = sessions_[mem[i].session_id];
     s.kv_len = std::max<int64_t>(s.kv_len, mem[i].history + mem[i].new_tokens);
   }
   submitted_ = true;
-  last_n_members_ = n;
+  return id;
 }
 
 void Instance::timer_record(int slot) {
@@ -750,7 +825,7 @@ double Instance::time_gemm(int layer, int which, int t_cap, int n_live, int iter
   const int qkv_out = (m_.n_q_heads + 2 * m_.n_kv_heads) * D;
   const SplitPlan sp = plan_for(t_cap, std::min(t_cap, r_max_));
   const LayerW& w = layers_[layer];
-  if (submitted_) lp_check(cudaEventSynchronize(ev_h2d_), "staging reuse");
+  acquire_staging();
   GemmArgs g;
   g.N = t_cap;
   g.n_dev = md_.scalars;
@@ -784,6 +859,7 @@ double Instance::time_gemm(int layer, int which, int t_cap, int n_live, int iter
   g.ntiles_dev = md_.scalars + 8;
   if (g.mode == kEpiF32Partial) g.splits_dev = md_.scalars + 4;
   lp_check(cudaMemcpyAsync(md_.scalars, mh_.scalars, 48, cudaMemcpyHostToDevice, stream_), "meta");
+  lp_check(cudaEventRecord(staging_[(stage_seq_ - 1) % kStaging].h2d, stream_), "event");
   lp_check(cudaStreamSynchronize(stream_), "sync");
   // Realistic operand values (unit-variance activations): an all-zero input
   // would under-state power draw and over-state the clock.
@@ -796,29 +872,22 @@ double Instance::time_gemm(int layer, int which, int t_cap, int n_live, int iter
   lp_check(cudaEventSynchronize(ev_end_), "sync");
   float ms = 0;
   lp_check(cudaEventElapsedTime(&ms, ev_start_, ev_end_), "elapsed");
-  submitted_ = false;  // lp_wait must not report this timing as a forward
   return ms / iters;
 }
 
 double Instance::wait() {
-  if (!submitted_) throw std::logic_error("lp_wait without a submit");
-  lp_check(cudaEventSynchronize(ev_end_), "forward");
-  float ms = 0;
-  lp_check(cudaEventElapsedTime(&ms, ev_start_, ev_end_), "elapsed");
-  return ms;
+  if (!submitted_) throw StateError("lp_wait without a submit");
+  return ticket_wait(next_ticket_ - 1);
 }
 
 void Instance::read_next_tokens(int32_t* out, int n) {
-  if (n > last_n_members_) throw ShapeMismatch("asked for more tokens than members");
-  std::vector<unsigned long long> keys(n);
-  lp_check(cudaMemcpyAsync(keys.data(), next_keys_, size_t(n) * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
-  lp_check(cudaStreamSynchronize(stream_), "d2h sync");
-  last_d2h_bytes_ = size_t(n) * 8;
-  for (int i = 0; i < n; ++i) out[i] = argmax_token(keys[i]);
+  if (!submitted_) throw StateError("lp_read_next_tokens without a submit");
+  ticket_tokens(next_ticket_ - 1, out, n);
 }
 
 void Instance::read_logits(float* out, size_t cap) {
-  const size_t need = size_t(last_n_members_) * m_.vocab;
+  if (!submitted_) throw StateError("lp_read_logits without a submit");
+  const size_t need = size_t(ticket(next_ticket_ - 1).n) * m_.vocab;
   if (cap < need) throw ShapeMismatch("logits buffer too small");
   lp_check(cudaMemcpyAsync(out, logits_, need * 4, cudaMemcpyDeviceToHost, stream_), "d2h");
   lp_check(cudaStreamSynchronize(stream_), "d2h sync");
@@ -870,7 +939,7 @@ void Instance::read_kv(int64_t sid, int layer, int64_t pos0, int64_t n, uint16_t
   }
 }
 
-void Instance::migrate(Instance& src, Instance& dst, int64_t sid) {
+void Instance::migrate(Instance& src, Instance& dst, int64_t sid, bool keep_source) {
   auto it = src.sessions_.find(sid);
   if (it == src.sessions_.end()) return;
   if (std::memcmp(&src.m_, &dst.m_, sizeof(lp_model_desc)) != 0) throw ConfigError("model mismatch");
@@ -898,8 +967,9 @@ void Instance::migrate(Instance& src, Instance& dst, int64_t sid) {
   if (peer) {
     // One kernel on the destination: reads the source pool directly (same
     // HBM, or the peer's HBM over NVLink) and writes the new pages.
-    // Page ids travel through the destination's pinned staging buffer (the
-    // sync below keeps it alive until the copy has read them).
+    // Page ids travel through the destination's pinned staging buffer; the
+    // previous incoming migration's H2D must have read it first.
+    if (dst.mig_pending_) lp_check(cudaEventSynchronize(dst.ev_mig_done_), "migration staging reuse");
     int* h = dst.mig_host_;
     for (int k = 0; k < n; ++k) {
       h[k] = ss.pages[k];
@@ -920,9 +990,14 @@ void Instance::migrate(Instance& src, Instance& dst, int64_t sid) {
       }
     }
   }
-  // The source may reuse the pages only after the copy read them.
-  lp_check(cudaStreamSynchronize(dst.stream_), "migrate sync");
-  src.session_release(sid);
+  // No host sync: the destination's next forwards are stream-ordered after
+  // the copy, and the source's stream waits for it before any later work of
+  // its own can reuse the released pages.
+  lp_check(cudaEventRecord(dst.ev_mig_done_, dst.stream_), "copy event");
+  dst.mig_pending_ = true;
+  lp_check(cudaSetDevice(src.d_.device), "set device");
+  lp_check(cudaStreamWaitEvent(src.stream_, dst.ev_mig_done_, 0), "src waits for copy");
+  if (!keep_source) src.session_release(sid);
 }
 
 }  // namespace lp
@@ -990,6 +1065,36 @@ int lp_submit(lp_instance* inst, const lp_shape* shape, const lp_member* members
   return lp::lp_guard([&] {
     if (!shape || !members || !token_ids) throw lp::ConfigError("null argument");
     impl_of(inst).submit(*shape, members, n, token_ids);
+  });
+}
+
+int lp_submit_async(lp_instance* inst, const lp_shape* shape, const lp_member* members, int32_t n,
+                    const int32_t* token_ids, int64_t* ticket) {
+  return lp::lp_guard([&] {
+    if (!shape || !members || !token_ids || !ticket) throw lp::ConfigError("null argument");
+    *ticket = -1;
+    *ticket = impl_of(inst).submit(*shape, members, n, token_ids);
+  });
+}
+
+int lp_ticket_query(lp_instance* inst, int64_t ticket, int32_t* done) {
+  return lp::lp_guard([&] {
+    if (!done) throw lp::ConfigError("null argument");
+    *done = impl_of(inst).ticket_done(ticket) ? 1 : 0;
+  });
+}
+
+int lp_ticket_wait(lp_instance* inst, int64_t ticket, double* service_ms) {
+  return lp::lp_guard([&] {
+    const double ms = impl_of(inst).ticket_wait(ticket);
+    if (service_ms) *service_ms = ms;
+  });
+}
+
+int lp_ticket_tokens(lp_instance* inst, int64_t ticket, int32_t* out, int32_t n) {
+  return lp::lp_guard([&] {
+    if (!out && n > 0) throw lp::ConfigError("null argument");
+    impl_of(inst).ticket_tokens(ticket, out, n);
   });
 }
 
@@ -1068,7 +1173,16 @@ int lp_session_migrate(lp_instance* src, lp_instance* dst, int64_t session_id) {
     Instance& a = impl_of(src);
     Instance& b = impl_of(dst);
     if (&a == &b) throw lp::ConfigError("lp_session_migrate: source and destination are the same instance");
-    Instance::migrate(a, b, session_id);
+    Instance::migrate(a, b, session_id, false);
+  });
+}
+
+int lp_session_copy(lp_instance* src, lp_instance* dst, int64_t session_id) {
+  return lp::lp_guard([&] {
+    Instance& a = impl_of(src);
+    Instance& b = impl_of(dst);
+    if (&a == &b) throw lp::ConfigError("lp_session_copy: source and destination are the same instance");
+    Instance::migrate(a, b, session_id, true);
   });
 }
 

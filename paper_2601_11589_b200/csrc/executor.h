@@ -78,14 +78,20 @@ class Instance {
   ~Instance();
 
   void capture_graphs(const std::vector<int64_t>& lens, const std::vector<int32_t>& depths);
-  void submit(const lp_shape& shape, const lp_member* members, int n, const int32_t* tokens);
-  double wait();
+  // Asynchronous: returns the ticket id of this forward (see Ticket).
+  int64_t submit(const lp_shape& shape, const lp_member* members, int n, const int32_t* tokens);
+  double wait();  // the last submit
   void read_next_tokens(int32_t* out, int n);
+  // Per-forward results (first tokens, device time) stay readable for the
+  // last kTickets submits; an older ticket is expired (LP_ERR_STATE).
+  bool ticket_done(int64_t id);
+  double ticket_wait(int64_t id);
+  void ticket_tokens(int64_t id, int32_t* out, int n);
   void read_logits(float* out, size_t cap);
   void session_pages(int64_t sid, int32_t* pages, int cap, int32_t* n_pages, int64_t* kv_len);
   void session_release(int64_t sid);
   void read_kv(int64_t sid, int layer, int64_t pos0, int64_t n, uint16_t* k, uint16_t* v);
-  static void migrate(Instance& src, Instance& dst, int64_t sid);
+  static void migrate(Instance& src, Instance& dst, int64_t sid, bool keep_source);
   void timer_record(int slot);
   double timer_elapsed(int a, int b);
   double time_gemm(int layer, int which, int t_cap, int n_live, int iters);
@@ -108,8 +114,36 @@ class Instance {
   lp_model_desc m_;
   lp_instance_desc d_;
   cudaStream_t stream_ = nullptr;
-  cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr, ev_h2d_ = nullptr;
-  cudaEvent_t ev_mig_ = nullptr;  // end of this instance's queued work, for a session migration
+  cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr;  // time_gemm only
+  cudaEvent_t ev_mig_ = nullptr;       // end of this instance's queued work, for a session migration
+  cudaEvent_t ev_mig_done_ = nullptr;  // an incoming migration's copy finished reading the ids
+  bool mig_pending_ = false;
+
+  // Host -> device metadata goes through kStaging pinned blocks used round
+  // robin, so the host can prepare forward k+1..k+3 while forward k runs;
+  // a block is rewritten only after its previous H2D copies drained.
+  static constexpr int kStaging = 4;
+  struct Staging {
+    void* host = nullptr;
+    Meta m{};
+    cudaEvent_t h2d = nullptr;
+    bool used = false;
+  };
+  Staging staging_[kStaging];
+  int64_t stage_seq_ = 0;
+  Meta& acquire_staging();  // points mh_ at the next free block
+  // One slot per in-flight forward: device-time events and a pinned copy of
+  // the greedy first tokens, written by a D2H at the end of the forward.
+  static constexpr int kTickets = 16;
+  struct Ticket {
+    int64_t id = -1;
+    int n = 0;
+    cudaEvent_t start = nullptr, end = nullptr, done = nullptr;
+    unsigned long long* keys = nullptr;  // pinned [r_max]
+  };
+  Ticket tickets_[kTickets];
+  int64_t next_ticket_ = 0;
+  Ticket& ticket(int64_t id);
 
   // model
   std::vector<LayerW> layers_;
@@ -143,7 +177,6 @@ class Instance {
   float* logits_ = nullptr;
   unsigned long long* next_keys_ = nullptr;
   void* meta_dev_ = nullptr;
-  void* meta_host_ = nullptr;
   int* mig_ids_ = nullptr;   // device page-id lists of an incoming migration
   int* mig_host_ = nullptr;  // pinned staging for them
   size_t meta_bytes_ = 0;
@@ -186,12 +219,10 @@ class Instance {
   // the warp-MMA kernel stays faster for short rows).
   std::map<int64_t, cudaGraphExec_t> graphs_tc_;
   int64_t graph_tc_pairs_ = 500000;  // LP_GRAPH_TC_PAIRS overrides
-  bool submitted_ = false;
+  bool submitted_ = false;  // a forward was submitted (lp_wait / lp_read_next_tokens refer to it)
  public:
   size_t last_h2d_bytes_ = 0, last_d2h_bytes_ = 0;  // host<->device bytes of the last submit / read
   int last_launches_ = 0;                             // kernels of the last submit
- private:
-  int last_n_members_ = 0;
 };
 
 }  // namespace lp

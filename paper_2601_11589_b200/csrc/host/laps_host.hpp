@@ -354,16 +354,37 @@ struct ForwardCall {
   std::vector<ForwardRow> rows;     // real members in plan order (no dummy rows)
   double model_service_ms = 0;      // what the reference cost model says
 };
+
+// How the engine's clock advances.
+//   kVirtual  discrete-event time: a forward completes clock_ms() after it
+//             was launched (the reference semantics; byte-identical logs).
+//   kWall     steady_clock time: arrivals are released in real time and a
+//             forward completes when poll() says so; lanes run concurrently.
+enum class TierClock { kVirtual, kWall };
+
+// Where dispatched forwards go. launch() must not block on the forward
+// itself, so several lanes (GPUs) overlap; a handle of 0 means "nothing to
+// wait for" (closed form).
 class ForwardBackend {
  public:
   virtual ~ForwardBackend() = default;
-  // Returns the service time the engine's clock advances by.
-  virtual double forward(const ForwardCall& call) = 0;
+  virtual std::uint64_t launch(const ForwardCall& call) = 0;
+  // Virtual clock: the service time the clock advances by (may block when it
+  // has to be measured).
+  virtual double clock_ms(std::uint64_t handle, const ForwardCall& call) = 0;
+  // Wall clock: true once the forward finished; *service_ms = its duration.
+  virtual bool poll(std::uint64_t handle, double* service_ms) = 0;
+  // The run is over: drain whatever is still queued.
+  virtual void finish_run() {}
 };
 // The reference semantics: service time = closed-form cost model.
 class CostModelBackend final : public ForwardBackend {
  public:
-  double forward(const ForwardCall& call) override { return call.model_service_ms; }
+  std::uint64_t launch(const ForwardCall&) override { return 0; }
+  double clock_ms(std::uint64_t, const ForwardCall& call) override { return call.model_service_ms; }
+  bool poll(std::uint64_t, double*) override {
+    throw std::logic_error("the closed-form backend has no wall-clock completions");
+  }
 };
 
 RunResult run(const SimConfig& sim, const std::vector<Request>& requests, const CostParams& cost,
@@ -373,6 +394,9 @@ RunResult run_with_backend(const SimConfig& sim, const std::vector<Request>& req
                            const CostParams& cost, const ExecOverheads& overheads,
                            const SchedConfig& sched, const GraphGrid& grid,
                            const ControllerConfig& ctrl, ForwardBackend& backend);
+RunResult run_tier(const SimConfig& sim, const std::vector<Request>& requests, const CostParams& cost,
+                   const ExecOverheads& overheads, const SchedConfig& sched, const GraphGrid& grid,
+                   const ControllerConfig& ctrl, ForwardBackend& backend, TierClock clock);
 
 // --------------------------------------------------------------- config.hpp
 using ConfigMap = std::map<std::string, std::string>;

@@ -14,7 +14,7 @@ from pathlib import Path
 from . import _native as N
 from .instance import PrefillInstance
 
-COST_MODEL, REPLAY, LIVE = 0, 1, 2
+COST_MODEL, REPLAY, LIVE, WALL = 0, 1, 2, 3
 
 
 class SimStats(ctypes.Structure):
@@ -24,10 +24,22 @@ class SimStats(ctypes.Structure):
                 ("active_ms", ctypes.c_double), ("ttft_mean_ms", ctypes.c_double),
                 ("ttft_p50_ms", ctypes.c_double), ("ttft_p90_ms", ctypes.c_double),
                 ("ttft_p99_ms", ctypes.c_double), ("rps", ctypes.c_double), ("slo_violation", ctypes.c_double),
-                ("gpu_ms_total", ctypes.c_double), ("engine_wall_s", ctypes.c_double)]
+                ("gpu_ms_total", ctypes.c_double), ("engine_wall_s", ctypes.c_double),
+                ("window_dispatches", ctypes.c_int64), ("window_requests", ctypes.c_int64),
+                ("window_fills", ctypes.c_int64), ("window_kernels", ctypes.c_int64),
+                ("window_h2d_bytes", ctypes.c_int64), ("window_d2h_bytes", ctypes.c_int64),
+                ("window_device_ms", ctypes.c_double), ("window_wall_ms", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class SimOpts(ctypes.Structure):
+    """lp_sim_opts: GPU dispatches [window_first, window_first + window_count)
+    form a timed window (REPLAY mode); stop_after_window runs later
+    dispatches on the clock only."""
+    _fields_ = [("window_first", ctypes.c_int64), ("window_count", ctypes.c_int64),
+                ("stop_after_window", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 def _declare():
@@ -37,6 +49,10 @@ def _declare():
         L.lp_sim_run.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int32,
                                  ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, ctypes.c_uint64,
                                  ctypes.POINTER(SimStats)]
+        L.lp_sim_run_ex.restype = ctypes.c_int32
+        L.lp_sim_run_ex.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int32,
+                                    ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, ctypes.c_uint64,
+                                    ctypes.POINTER(SimOpts), ctypes.POINTER(SimStats)]
         L.lp_sim_sweep.restype = ctypes.c_int32
         L.lp_sim_sweep.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int32,
                                    ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, ctypes.c_uint64,
@@ -69,15 +85,19 @@ def read_config(path: str | Path) -> str:
 
 
 def simulate(config_text: str, overrides: str | dict = "", out_dir: str | Path = "", mode: int = COST_MODEL,
-             instances: list[PrefillInstance] | None = None, token_seed: int = 7) -> SimStats:
+             instances: list[PrefillInstance] | None = None, token_seed: int = 7,
+             window: tuple[int, int] | None = None, stop_after_window: bool = True) -> SimStats:
+    """One engine run (lp_sim_run_ex). `window=(first, count)` times GPU
+    dispatches [first, first + count) of a REPLAY run (window_* stats)."""
     if isinstance(overrides, dict):
         overrides = "".join(f"{k} = {v}\n" for k, v in overrides.items())
     L = _declare()
     insts = instances or []
     arr = (ctypes.c_void_p * max(1, len(insts)))(*[i._h.value for i in insts])
     st = SimStats()
-    N.check(L.lp_sim_run(config_text.encode(), overrides.encode(), str(out_dir).encode(), mode,
-                         arr if insts else None, len(insts), token_seed, ctypes.byref(st)))
+    opts = SimOpts(window[0], window[1], 1 if stop_after_window else 0, 0) if window else SimOpts()
+    N.check(L.lp_sim_run_ex(config_text.encode(), overrides.encode(), str(out_dir).encode(), mode,
+                            arr if insts else None, len(insts), token_seed, ctypes.byref(opts), ctypes.byref(st)))
     return st
 
 

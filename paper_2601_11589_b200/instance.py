@@ -140,6 +140,33 @@ class PrefillInstance:
                                  toks.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
         self._last_n = len(members)
 
+    def submit_async(self, l_pad: int, depth: int, kind: int, members: list[Member], token_ids: np.ndarray) -> int:
+        """Queue a forward without waiting; returns its ticket (lp_submit_async)."""
+        shape = N.Shape(l_pad, depth, kind)
+        arr = (N.Member * len(members))(*[N.Member(m.req_id, m.session_id, m.new_tokens, m.history, 1, 0)
+                                          for m in members])
+        toks = np.ascontiguousarray(token_ids, dtype=np.int32)
+        t = ctypes.c_int64()
+        _check(N.lib().lp_submit_async(self._h, ctypes.byref(shape), arr, len(members),
+                                       toks.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ctypes.byref(t)))
+        self._last_n = len(members)
+        return t.value
+
+    def ticket_done(self, ticket: int) -> bool:
+        d = ctypes.c_int32()
+        _check(N.lib().lp_ticket_query(self._h, ticket, ctypes.byref(d)))
+        return bool(d.value)
+
+    def ticket_wait(self, ticket: int) -> float:
+        ms = ctypes.c_double()
+        _check(N.lib().lp_ticket_wait(self._h, ticket, ctypes.byref(ms)))
+        return ms.value
+
+    def ticket_tokens(self, ticket: int, n: int) -> np.ndarray:
+        out = np.empty(n, dtype=np.int32)
+        _check(N.lib().lp_ticket_tokens(self._h, ticket, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n))
+        return out
+
     def wait(self) -> float:
         ms = ctypes.c_double()
         _check(N.lib().lp_wait(self._h, ctypes.byref(ms)))
