@@ -144,7 +144,7 @@ class GpuTier final : public ForwardBackend {
 
   void write(const std::string& dir) const {
     std::ofstream out(dir + "/forwards.csv");
-    out << "inst,kind,l_pad,depth,graph,members,tokens,hist_tokens,attn_pairs,model_ms,gpu_ms\n";
+    out << "inst,kind,l_pad,depth,graph,members,tokens,hist_tokens,attn_pairs,model_ms,gpu_ms,window,finished\n";
     std::ofstream first(dir + "/first_tokens.csv");
     first << "req,token\n";
     std::vector<std::pair<RequestId, int32_t>> firsts;
@@ -153,7 +153,9 @@ class GpuTier final : public ForwardBackend {
       const ForwardCall& c = f.call;
       out << c.inst << ',' << static_cast<int>(c.kind) << ',' << c.shape.l_pad << ',' << c.shape.depth << ','
           << (c.shape.kind == ShapeKind::kGraph ? 1 : 0) << ',' << c.rows.size() << ',' << f.tokens << ','
-          << f.hist << ',' << f.pairs << ',' << c.model_service_ms << ',' << f.gpu_ms << '\n';
+          << f.hist << ',' << f.pairs << ',' << c.model_service_ms << ',' << f.gpu_ms << ',' << (f.in_window ? 1 : 0)
+          << ',' << std::count_if(c.rows.begin(), c.rows.end(), [](const ForwardRow& r) { return r.finishes_request; })
+          << '\n';
       for (size_t i = 0; i < c.rows.size() && i < f.first.size(); ++i)
         if (c.rows[i].finishes_request) firsts.emplace_back(c.rows[i].req_id, f.first[i]);
     }

@@ -1,16 +1,19 @@
-"""Multi-instance (N > 1) host logic on CPU with world_size-2 gloo.
+"""Multi-GPU (N > 1) host logic on CPU with world_size-2 gloo.
 
-Each rank is an independent prefill instance behind the length-aware router
-(spatial disaggregation: no collective on the data path). Every rank runs the
-host engine on its own request stream (seed 41 + rank, as bench.py does), and
-the job-level numbers use bench.py's own aggregation: requests summed over
-ranks, time = max over ranks. The test checks that against each rank's
-single-process result."""
+bench.py under torchrun: rank 0 drives every GPU from one host engine (the
+reference's length-aware router is global, sim.cpp:379-411) and the other
+ranks only join the barriers. Here rank 0 runs bench.scenario(2, ...) — the
+2-GPU spatial configuration — on the wall-clock engine with paced (sleeping)
+forwards, rank 1 idles, and the test checks the spatial split: short work on
+the short-pool instance, long chunks on the long-pool one, both busy at the
+same time, plus the window accounting bench.py reports."""
+import json
 import os
 import socket
+import tempfile
+from pathlib import Path
 
 import pytest
-import torch.distributed as dist
 import torch.multiprocessing as mp
 
 
@@ -21,31 +24,47 @@ def _free_port() -> int:
 
 
 def _worker(rank: int, ws: int, port: int, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(ws), RANK=str(rank))
     import bench
-    from paper_2601_11589_b200 import engine as E
-    from paper_2601_11589_b200 import scenarios as S
-    cfg = bench.scenario(rank, lam=0.3, dur=3000)
-    st = E.simulate(S.text(cfg))  # cost-model clock: deterministic per rank
-    value, total, t_max = bench.aggregate_throughput(dist, st.completed, st.active_ms, rank)
-    q.put((rank, st.completed, st.active_ms, value, total, t_max))
+    dist = bench.dist_init(ws)
+    bench.barrier(dist)
+    if rank == 0:
+        from paper_2601_11589_b200 import engine as E
+        from paper_2601_11589_b200 import scenarios as S
+        cfg = bench.scenario(2, 0.01, 1200)
+        out = Path(tempfile.mkdtemp())
+        st = E.simulate(S.text(cfg), "", out, mode=E.WALL)
+        recs = [json.loads(x) for x in (out / "events.log").read_text().splitlines()]
+        q.put((rank, st.arrivals, st.completed, recs, cfg))
+    else:
+        q.put((rank, 0, 0, [], {}))
+    bench.barrier(dist)
     dist.destroy_process_group()
 
 
-def test_two_rank_aggregation():
+def test_two_rank_spatial_router():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=120) for _ in procs)
+    res = sorted((q.get(timeout=300) for _ in procs), key=lambda x: x[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (r0, c0, a0, v0, tot0, tm0), (r1, c1, a1, v1, tot1, tm1) = res
-    assert c0 > 0 and c1 > 0 and c0 != c1           # independent streams
-    assert tot0 == tot1 == c0 + c1
-    assert tm0 == tm1 == max(a0, a1)
-    assert v0 == pytest.approx((c0 + c1) / (max(a0, a1) / 1000.0))
+    _, arrivals, completed, recs, cfg = res[0]
+    assert cfg["sim.disagg"] == "spatial" and cfg["sim.instances"] == "2"
+    assert arrivals > 0 and completed == arrivals
+    disp = [r for r in recs if r["kind"] == "dispatch"]
+    assert {r["inst"] for r in disp if r["reason"] != "long_chunk"} == {0}   # short pool
+    assert {r["inst"] for r in disp if r["reason"] == "long_chunk"} == {1}   # long pool
+    assert res[1][1] == 0  # rank 1 did no work
+
+
+def test_window_accounting():
+    import bench
+    disp = [{"reason": "long_chunk", "chunk": 1, "chunks": 4, "reqs": [3]},
+            {"reason": "depth_reached", "reqs": [5, 6]},
+            {"reason": "long_chunk", "chunk": 4, "chunks": 4, "reqs": [3]}]
+    assert bench.request_equivalents(disp) == pytest.approx(2.5)
