@@ -458,6 +458,9 @@ def run_ours(args) -> None:
         "setup_s": setup_s,
     }
     print(json.dumps(result), flush=True)
+    if os.environ.get("LP_BENCH_OUT"):  # keep events.log / forwards.csv of the run (profiling)
+        import shutil
+        shutil.copytree(work, os.environ["LP_BENCH_OUT"], dirs_exist_ok=True)
     for inst in insts:
         inst.close()
     barrier(dist)
