@@ -1,7 +1,14 @@
-// Closed-form pieces of the host engine: the analytical service-time model
-// (the forward stand-in, cost_model.cpp:36-61, 128-158) and the Alg. 2
-// controller arithmetic (controller.cpp:9-65). Expression order follows the
-// reference term by term so double results are bit-identical.
+// Closed-form parts of the host engine.
+//
+//  * The Alg. 2 pool controller's arithmetic (reference controller.cpp:9-65):
+//    per-instance pressure, the percentile aggregate of a pool, the
+//    hysteresis / cool-down / minimum-pool decision.
+//  * The analytical service-time model the reference uses in place of a
+//    forward (cost_model.cpp:36-61, 128-158). It still drives the REPLAY
+//    clock (so batch composition matches the reference) and the cost-model
+//    mode; on the GPU path the real forward replaces it. The floating-point
+//    expressions are the reference's term for term (the clock must be
+//    bit-identical), the surrounding code is this repo's own.
 #include <algorithm>
 #include <cmath>
 
@@ -9,115 +16,157 @@
 
 namespace laps {
 
-void validate(const CostParams& p) {
-  if (!(p.alpha > 0) || !std::isfinite(p.alpha)) throw ConfigError("cost.alpha must be finite and > 0");
-  for (double v : {p.beta, p.gamma_w, p.gamma_r})
-    if (v < 0 || !std::isfinite(v)) throw ConfigError("cost coefficients must be finite and >= 0");
+namespace {
+
+struct Rule {
+  bool broken;
+  const char* why;
+};
+void enforce(std::initializer_list<Rule> rules) {
+  for (const Rule& r : rules)
+    if (r.broken) throw ConfigError(r.why);
 }
 
-void validate(const ExecOverheads& o) {
-  if (!(o.eta > 0) || o.eta > 1.0) throw ConfigError("cost.eta must be in (0,1]");
-  if (o.kappa_graph_ms < 0 || o.kappa_std_ms < o.kappa_graph_ms)
-    throw ConfigError("need 0 <= kappa_graph <= kappa_std");
-}
+bool finite_positive(double v) { return v > 0 && std::isfinite(v); }
+bool finite_nonnegative(double v) { return v >= 0 && std::isfinite(v); }
 
-void validate(const RooflineParams& r) {
-  for (double v : {r.p_peak, r.b_mem, r.bytes_per_token, r.ops_per_token})
-    if (!(v > 0) || !std::isfinite(v)) throw ConfigError("roofline parameters must be finite and > 0");
-}
+}  // namespace
 
-LatencyTerms compute_latency(double L, double H, const CostParams& p) {
-  // t_comp = alpha*L*(L+2H) + beta*L ; t_mem = gamma_w*L + gamma_r*H
-  return LatencyTerms{p.alpha * L * (L + 2.0 * H) + p.beta * L, p.gamma_w * L + p.gamma_r * H};
+// ---------------------------------------------------------------- controller
+int PoolState::n_long() const {
+  int n = 0;
+  for (PoolKind k : assignment) n += k == PoolKind::kLong ? 1 : 0;
+  return n;
 }
-
-double prefill_boundary(const CostParams& p) { return std::max(0.0, (p.gamma_w - p.beta) / p.alpha); }
-
-double reprefill_boundary(const CostParams& p, double H) {
-  // Nonnegative root of alpha*L^2 + b*L - gamma_r*H with b = 2*alpha*H + beta - gamma_w;
-  // the rationalised form is used when b >= 0 to avoid cancellation.
-  const double b = 2.0 * p.alpha * H + p.beta - p.gamma_w;
-  const double sq = std::sqrt(b * b + 4.0 * p.alpha * p.gamma_r * H);
-  const double root = b >= 0 ? ((b + sq) > 0 ? 2.0 * p.gamma_r * H / (b + sq) : 0.0)
-                             : (-b + sq) / (2.0 * p.alpha);
-  return std::max(0.0, root);
-}
-
-double batch_service_time(const BatchShape& shape, std::span<const MemberShape> members,
-                          const CostParams& p, const ExecOverheads& o) {
-  if (static_cast<int>(members.size()) != shape.depth) {
-    throw ShapeMismatch("member count " + std::to_string(members.size()) + " != shape depth " +
-                        std::to_string(shape.depth));
-  }
-  double acc = 0;
-  for (const auto& m : members) {
-    if (m.first > shape.l_pad) {
-      throw ShapeMismatch("member length " + std::to_string(m.first) + " exceeds l_pad " +
-                          std::to_string(shape.l_pad));
-    }
-    // Padding is billed in full: every row costs a full l_pad row.
-    acc += compute_latency(static_cast<double>(shape.l_pad), static_cast<double>(m.second), p).total_ms();
-  }
-  const double kappa = shape.kind == ShapeKind::kGraph ? o.kappa_graph_ms : o.kappa_std_ms;
-  return kappa + std::pow(static_cast<double>(shape.depth), o.eta - 1.0) * acc;
-}
-
-double packed_service_time(std::span<const MemberShape> members, const CostParams& p,
-                           const ExecOverheads& o) {
-  double acc = 0;
-  for (const auto& m : members)
-    acc += compute_latency(static_cast<double>(m.first), static_cast<double>(m.second), p).total_ms();
-  return o.kappa_std_ms + acc;
-}
-
-// ------------------------------------------------------------- controller
-int PoolState::n_short() const {
-  return static_cast<int>(std::count(assignment.begin(), assignment.end(), PoolKind::kShort));
-}
-int PoolState::n_long() const { return static_cast<int>(assignment.size()) - n_short(); }
+int PoolState::n_short() const { return static_cast<int>(assignment.size()) - n_long(); }
 
 const char* to_string(MigrationDir d) {
-  return d == MigrationDir::kLongToShort ? "long_to_short" : "short_to_long";
+  switch (d) {
+    case MigrationDir::kShortToLong: return "short_to_long";
+    case MigrationDir::kLongToShort: return "long_to_short";
+  }
+  return "?";
 }
 
-void validate(const ControllerConfig& cfg, int n_instances) {
-  if (!(cfg.dt_ms > 0)) throw ConfigError("control period must be > 0");
-  if (cfg.t_cool_ms < 0) throw ConfigError("cool-down must be >= 0");
-  if (cfg.tau_hyst < 0) throw ConfigError("hysteresis must be >= 0");
-  if (cfg.n_min < 0) throw ConfigError("n_min must be >= 0");
-  if (2 * cfg.n_min > n_instances) throw ConfigError("n_min * 2 exceeds the instance count");
-  for (double w : {cfg.w_q, cfg.w_e, cfg.w_u})
-    if (w < 0) throw ConfigError("pressure weights must be >= 0");
-  if (cfg.aggregator_percentile < 1 || cfg.aggregator_percentile > 100)
-    throw ConfigError("aggregator percentile must be in [1, 100]");
+void validate(const ControllerConfig& c, int n_instances) {
+  enforce({
+      {!(c.dt_ms > 0), "ctrl.dt_ms must be > 0"},
+      {c.t_cool_ms < 0, "ctrl.t_cool_ms must be >= 0"},
+      {c.tau_hyst < 0, "ctrl.tau_hyst must be >= 0"},
+      {c.n_min < 0, "ctrl.n_min must be >= 0"},
+      {c.n_min * 2 > n_instances, "ctrl.n_min leaves no room for two pools of that size"},
+      {c.w_q < 0 || c.w_e < 0 || c.w_u < 0, "ctrl weights w_q, w_e, w_u must be >= 0"},
+      {c.aggregator_percentile < 1 || c.aggregator_percentile > 100, "ctrl percentile must be in 1..100"},
+  });
 }
 
-double pressure(const InstanceStats& s, const ControllerConfig& cfg) {
-  return cfg.w_q * s.q + cfg.w_e * s.e - cfg.w_u * s.u;
+// Queue pressure plus lateness, minus how busy the instance already is.
+double pressure(const InstanceStats& s, const ControllerConfig& c) {
+  return c.w_q * s.q + c.w_e * s.e - c.w_u * s.u;
 }
 
+// Pool score: the nearest-rank p-th percentile of its instances' pressures,
+// rank ceil(p n / 100) computed in integers.
 double aggregate(std::span<const double> scores, int pct) {
   if (scores.empty()) throw EmptyPool();
+  const size_t n = scores.size();
+  size_t rank = (static_cast<size_t>(pct) * n + 99) / 100;
+  rank = std::min(std::max<size_t>(rank, 1), n);
   std::vector<double> v(scores.begin(), scores.end());
-  std::sort(v.begin(), v.end());
-  // nearest rank ceil(p*n/100) in integer arithmetic
-  const size_t n = v.size();
-  const size_t rank = std::clamp<size_t>((static_cast<size_t>(pct) * n + 99) / 100, 1, n);
+  std::nth_element(v.begin(), v.begin() + static_cast<long>(rank - 1), v.end());
   return v[rank - 1];
 }
 
-std::optional<MigrationDir> decide(double p_s, double p_l, PoolState& st, const ControllerConfig& cfg,
+// Move one instance toward the pool under more pressure, when it is ahead
+// by the hysteresis margin, the donor pool keeps n_min instances, and the
+// last move is at least t_cool ago.
+std::optional<MigrationDir> decide(double p_s, double p_l, PoolState& pools, const ControllerConfig& c,
                                    double now) {
-  if (now - st.t_last_ms < cfg.t_cool_ms) return std::nullopt;
-  const double gain = 1.0 + cfg.tau_hyst;
-  std::optional<MigrationDir> dir;
-  if (p_s > gain * p_l && st.n_long() > cfg.n_min) {
-    dir = MigrationDir::kLongToShort;
-  } else if (p_l > gain * p_s && st.n_short() > cfg.n_min) {
-    dir = MigrationDir::kShortToLong;
+  if (now - pools.t_last_ms < c.t_cool_ms) return std::nullopt;
+  const double margin = 1.0 + c.tau_hyst;
+  const bool short_starved = p_s > margin * p_l && pools.n_long() > c.n_min;
+  const bool long_starved = !short_starved && p_l > margin * p_s && pools.n_short() > c.n_min;
+  if (!short_starved && !long_starved) return std::nullopt;
+  pools.t_last_ms = now;
+  return short_starved ? MigrationDir::kLongToShort : MigrationDir::kShortToLong;
+}
+
+// ---------------------------------------------------------------- cost model
+void validate(const RooflineParams& r) {
+  enforce({{!finite_positive(r.p_peak) || !finite_positive(r.b_mem) || !finite_positive(r.bytes_per_token) ||
+                !finite_positive(r.ops_per_token),
+            "roofline parameters must be finite and > 0"}});
+}
+
+void validate(const ExecOverheads& o) {
+  enforce({
+      {!(o.eta > 0) || o.eta > 1.0, "exec.eta must lie in (0, 1]"},
+      {o.kappa_graph_ms < 0 || o.kappa_std_ms < o.kappa_graph_ms, "exec: need 0 <= kappa_graph <= kappa_std"},
+  });
+}
+
+void validate(const CostParams& p) {
+  enforce({
+      {!finite_positive(p.alpha), "cost.alpha must be finite and > 0"},
+      {!finite_nonnegative(p.beta) || !finite_nonnegative(p.gamma_w) || !finite_nonnegative(p.gamma_r),
+       "cost.beta, cost.gamma_w, cost.gamma_r must be finite and >= 0"},
+  });
+}
+
+// One row of L new tokens over H cached ones: compute (quadratic attention
+// + linear projections) and memory (KV write + KV read) terms.
+LatencyTerms compute_latency(double L, double H, const CostParams& p) {
+  LatencyTerms t;
+  t.comp_ms = p.alpha * L * (L + 2.0 * H) + p.beta * L;
+  t.mem_ms = p.gamma_w * L + p.gamma_r * H;
+  return t;
+}
+
+// L at which a fresh prompt's compute time overtakes its memory time.
+double prefill_boundary(const CostParams& p) {
+  const double crossing = (p.gamma_w - p.beta) / p.alpha;
+  return crossing > 0.0 ? crossing : 0.0;
+}
+
+// Same crossing for a re-prefill over H cached tokens: the nonnegative root
+// of alpha L^2 + b L - gamma_r H = 0, b = 2 alpha H + beta - gamma_w, in the
+// cancellation-free form when b >= 0.
+double reprefill_boundary(const CostParams& p, double H) {
+  const double b = 2.0 * p.alpha * H + p.beta - p.gamma_w;
+  const double disc = std::sqrt(b * b + 4.0 * p.alpha * p.gamma_r * H);
+  double L = 0.0;
+  if (b < 0) L = (-b + disc) / (2.0 * p.alpha);
+  else if (b + disc > 0) L = 2.0 * p.gamma_r * H / (b + disc);
+  return L > 0.0 ? L : 0.0;
+}
+
+// A padded batch: every row is billed as a full l_pad row (dummy rows up to
+// the depth too), the sum scaled by depth^(eta - 1), plus the launch cost of
+// a graph replay or an eager launch.
+double batch_service_time(const BatchShape& shape, std::span<const MemberShape> members, const CostParams& p,
+                          const ExecOverheads& o) {
+  if (members.size() != static_cast<size_t>(std::max(shape.depth, 0)) || shape.depth < 0)
+    throw ShapeMismatch("batch of " + std::to_string(members.size()) + " rows for a graph of depth " +
+                        std::to_string(shape.depth));
+  const double row_len = static_cast<double>(shape.l_pad);
+  double rows_ms = 0;
+  for (const MemberShape& m : members) {
+    if (m.first > shape.l_pad)
+      throw ShapeMismatch("row of " + std::to_string(m.first) + " tokens does not fit l_pad " +
+                          std::to_string(shape.l_pad));
+    rows_ms += compute_latency(row_len, static_cast<double>(m.second), p).total_ms();
   }
-  if (dir) st.t_last_ms = now;
-  return dir;
+  const double launch = shape.kind == ShapeKind::kGraph ? o.kappa_graph_ms : o.kappa_std_ms;
+  const double batching = std::pow(static_cast<double>(shape.depth), o.eta - 1.0);
+  return launch + batching * rows_ms;
+}
+
+// The FCFS baseline's packed batch: no padding, no batching discount.
+double packed_service_time(std::span<const MemberShape> members, const CostParams& p, const ExecOverheads& o) {
+  double rows_ms = 0;
+  for (const MemberShape& m : members)
+    rows_ms += compute_latency(static_cast<double>(m.first), static_cast<double>(m.second), p).total_ms();
+  return o.kappa_std_ms + rows_ms;
 }
 
 }  // namespace laps

@@ -85,132 +85,134 @@ void write_event_log(const std::string& path, std::span<const LogRecord> log) {
 }
 
 // ------------------------------------------------------------------ metrics
+// Nearest-rank percentile: the ceil(q n / 100)-th smallest sample (the 1e-9
+// keeps 0.9 * 10 from rounding up to rank 10).
 double percentile(std::span<const double> samples, double q) {
   if (samples.empty()) throw EmptySamples();
-  if (!(q > 0) || q > 100) throw std::invalid_argument("percentile rank must be in (0, 100]");
+  if (!(q > 0 && q <= 100)) throw std::invalid_argument("percentile: q must lie in (0, 100]");
   std::vector<double> v(samples.begin(), samples.end());
-  std::sort(v.begin(), v.end());
-  // rank = ceil(q*n/100), nudged so 0.9*10 does not round up to 10.
   const double n = static_cast<double>(v.size());
-  const size_t rank = std::clamp<size_t>(static_cast<size_t>(std::ceil(q * n / 100.0 - 1e-9)), 1, v.size());
+  size_t rank = static_cast<size_t>(std::ceil(q * n / 100.0 - 1e-9));
+  rank = std::min(std::max<size_t>(rank, 1), v.size());
+  std::nth_element(v.begin(), v.begin() + static_cast<long>(rank - 1), v.end());
   return v[rank - 1];
 }
 
 double slo_violation_rate(std::span<const double> t, double slo_ms) {
   if (t.empty()) throw EmptySamples();
-  std::int64_t over = 0;
-  for (double x : t) over += x > slo_ms ? 1 : 0;
-  return static_cast<double>(over) / static_cast<double>(t.size());
+  const auto late = std::count_if(t.begin(), t.end(), [&](double x) { return x > slo_ms; });
+  return static_cast<double>(late) / static_cast<double>(t.size());
 }
 
 namespace {
 
-struct Tally {
-  std::int64_t batches = 0, graph = 0, depth = 0;
+// Everything one class (overall / short / long) contributes to metrics.json.
+struct ClassBook {
+  std::vector<double> ttft, wait;  // per request, in arrival order
+  std::int64_t batches = 0, graph_batches = 0, members = 0;
   Tokens real = 0, padded = 0;
-  void add(const LogRecord& r) {
-    ++batches;
-    graph += r.graph ? 1 : 0;
-    depth += static_cast<std::int64_t>(r.reqs.size());
+
+  void batch(const LogRecord& r) {
+    batches += 1;
+    graph_batches += r.graph ? 1 : 0;
+    members += static_cast<std::int64_t>(r.reqs.size());
     real += r.real_tokens;
     padded += r.padded_tokens;
   }
+
+  static double mean(const std::vector<double>& v) {
+    double acc = 0;
+    for (double x : v) acc += x;
+    return acc / static_cast<double>(v.size());
+  }
+
+  ClassMetrics finish(double slo_ms, double active_ms) const {
+    ClassMetrics m;
+    m.completed = static_cast<std::int64_t>(ttft.size());
+    m.batches = batches;
+    if (!ttft.empty()) {
+      m.ttft_mean_ms = mean(ttft);
+      m.ttft_p50_ms = percentile(ttft, 50);
+      m.ttft_p90_ms = percentile(ttft, 90);
+      m.ttft_p99_ms = percentile(ttft, 99);
+      m.slo_violation = slo_violation_rate(ttft, slo_ms);
+      if (active_ms > 0) m.rps = 1000.0 * static_cast<double>(m.completed) / active_ms;
+    }
+    if (!wait.empty()) m.mean_wait_ms = mean(wait);
+    if (batches > 0) {
+      const double nb = static_cast<double>(batches);
+      m.mean_depth = static_cast<double>(members) / nb;
+      m.graph_hit_rate = static_cast<double>(graph_batches) / nb;
+    }
+    if (real > 0) m.padding_overhead = static_cast<double>(padded) / static_cast<double>(real) - 1.0;
+    return m;
+  }
 };
 
-ClassMetrics summarise(const std::vector<double>& ttft, const std::vector<double>& wait, const Tally& b,
-                       double slo_ms, double active_ms) {
-  ClassMetrics m;
-  m.completed = static_cast<std::int64_t>(ttft.size());
-  if (!ttft.empty()) {
-    double sum = 0;
-    for (double t : ttft) sum += t;
-    m.ttft_mean_ms = sum / static_cast<double>(ttft.size());
-    m.ttft_p50_ms = percentile(ttft, 50);
-    m.ttft_p90_ms = percentile(ttft, 90);
-    m.ttft_p99_ms = percentile(ttft, 99);
-    m.slo_violation = slo_violation_rate(ttft, slo_ms);
-    if (active_ms > 0) m.rps = 1000.0 * static_cast<double>(m.completed) / active_ms;
-  }
-  if (!wait.empty()) {
-    double sum = 0;
-    for (double w : wait) sum += w;
-    m.mean_wait_ms = sum / static_cast<double>(wait.size());
-  }
-  m.batches = b.batches;
-  if (b.batches > 0) {
-    m.mean_depth = static_cast<double>(b.depth) / static_cast<double>(b.batches);
-    m.graph_hit_rate = static_cast<double>(b.graph) / static_cast<double>(b.batches);
-  }
-  if (b.real > 0) m.padding_overhead = static_cast<double>(b.padded) / static_cast<double>(b.real) - 1.0;
-  return m;
-}
+// One request's milestones on the log's clock (-1 = never happened).
+struct Milestones {
+  double arrived = 0, dispatched = -1, finished = -1;
+  bool is_long = false;
+};
 
 }  // namespace
 
+// Metrics are recomputed from the event log alone (the log is the contract):
+// arrivals open a request, its first dispatch ends its wait, the completion
+// of its final chunk ends its TTFT; RPS counts completions over the span
+// from the first arrival to the last completion.
 MetricsReport metrics_from_log(std::span<const LogRecord> log, double slo_ms) {
-  struct Info {
-    double arrival = 0, first_dispatch = -1, completion = -1;
-    bool is_long = false;
-  };
+  std::vector<Milestones> reqs;                  // arrival order
+  std::unordered_map<RequestId, size_t> where;  // request id -> reqs index
+  ClassBook all, shorts, longs;
   MetricsReport rep;
   rep.slo_ms = slo_ms;
-  std::unordered_map<RequestId, Info> info;
-  std::vector<RequestId> order;
-  Tally all, shorts, longs;
-  double first_arrival = std::numeric_limits<double>::infinity();
-  double last_completion = -std::numeric_limits<double>::infinity();
-  for (const auto& r : log) {
-    switch (r.kind) {
-      case EventKind::kArrival:
-        info[r.req] = Info{r.t, -1, -1, r.cls == "long"};
-        order.push_back(r.req);
-        rep.arrivals += 1;
-        first_arrival = std::min(first_arrival, r.t);
-        break;
-      case EventKind::kDispatch:
-        for (RequestId id : r.reqs) {
-          auto it = info.find(id);
-          if (it != info.end() && it->second.first_dispatch < 0) it->second.first_dispatch = r.t;
-        }
-        all.add(r);
-        if (r.cls == "short") shorts.add(r);
-        if (r.cls == "long") longs.add(r);
-        break;
-      case EventKind::kBatchComplete:
-        if (!r.final_chunk) break;
-        for (RequestId id : r.reqs) {
-          auto it = info.find(id);
-          if (it != info.end()) {
-            it->second.completion = r.t;
-            last_completion = std::max(last_completion, r.t);
-          }
-        }
-        break;
-      case EventKind::kMigration:
-        rep.migrations += 1;
-        break;
-      case EventKind::kControllerTick:
-        break;
+  bool seen_arrival = false, seen_completion = false;
+  double t_first = 0, t_last = 0;
+  auto milestones = [&](RequestId id) -> Milestones* {
+    const auto it = where.find(id);
+    return it == where.end() ? nullptr : &reqs[it->second];
+  };
+  for (const LogRecord& r : log) {
+    if (r.kind == EventKind::kArrival) {
+      where[r.req] = reqs.size();
+      reqs.push_back(Milestones{r.t, -1, -1, r.cls == "long"});
+      rep.arrivals += 1;
+      t_first = seen_arrival ? std::min(t_first, r.t) : r.t;
+      seen_arrival = true;
+    } else if (r.kind == EventKind::kDispatch) {
+      for (RequestId id : r.reqs)
+        if (Milestones* m = milestones(id); m && m->dispatched < 0) m->dispatched = r.t;
+      all.batch(r);
+      if (r.cls == "short") shorts.batch(r);
+      else if (r.cls == "long") longs.batch(r);
+    } else if (r.kind == EventKind::kBatchComplete && r.final_chunk) {
+      for (RequestId id : r.reqs) {
+        Milestones* m = milestones(id);
+        if (!m) continue;
+        m->finished = r.t;
+        t_last = seen_completion ? std::max(t_last, r.t) : r.t;
+        seen_completion = true;
+      }
+    } else if (r.kind == EventKind::kMigration) {
+      rep.migrations += 1;
     }
   }
-  if (std::isfinite(first_arrival) && last_completion > first_arrival) rep.active_ms = last_completion - first_arrival;
-  std::vector<double> t_all, t_s, t_l, w_all, w_s, w_l;
-  for (RequestId id : order) {  // arrival order keeps double sums reproducible
-    const Info& ri = info.at(id);
-    if (ri.completion >= 0) {
-      const double t = ri.completion - ri.arrival;
-      t_all.push_back(t);
-      (ri.is_long ? t_l : t_s).push_back(t);
+  if (seen_arrival && seen_completion && t_last > t_first) rep.active_ms = t_last - t_first;
+  for (const Milestones& m : reqs) {
+    ClassBook& cls = m.is_long ? longs : shorts;
+    if (m.finished >= 0) {
+      all.ttft.push_back(m.finished - m.arrived);
+      cls.ttft.push_back(m.finished - m.arrived);
     }
-    if (ri.first_dispatch >= 0) {
-      const double w = ri.first_dispatch - ri.arrival;
-      w_all.push_back(w);
-      (ri.is_long ? w_l : w_s).push_back(w);
+    if (m.dispatched >= 0) {
+      all.wait.push_back(m.dispatched - m.arrived);
+      cls.wait.push_back(m.dispatched - m.arrived);
     }
   }
-  rep.overall = summarise(t_all, w_all, all, slo_ms, rep.active_ms);
-  rep.short_cls = summarise(t_s, w_s, shorts, slo_ms, rep.active_ms);
-  rep.long_cls = summarise(t_l, w_l, longs, slo_ms, rep.active_ms);
+  rep.overall = all.finish(slo_ms, rep.active_ms);
+  rep.short_cls = shorts.finish(slo_ms, rep.active_ms);
+  rep.long_cls = longs.finish(slo_ms, rep.active_ms);
   return rep;
 }
 
