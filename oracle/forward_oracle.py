@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import subprocess
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -58,6 +59,7 @@ def synth_lib() -> ctypes.CDLL:
         _synth.oracle_weights_bf16.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                                ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64,
                                                ctypes.c_float, ctypes.c_int]
+        _synth.oracle_weights_bf16_mt.argtypes = _synth.oracle_weights_bf16.argtypes + [ctypes.c_int]
     return _synth
 
 
@@ -72,8 +74,8 @@ def weight_bf16(rows: int, cols: int, seed: int, tid: int, scale: float, interle
     """bf16 weight tensor (as torch.bfloat16) from the counter-based generator."""
     nrows = rows if nrows is None else nrows
     buf = np.empty((nrows, cols), dtype=np.uint16)
-    synth_lib().oracle_weights_bf16(buf.ctypes.data, row0, nrows, cols, seed, tid, ctypes.c_float(scale),
-                                    1 if interleave else 0)
+    synth_lib().oracle_weights_bf16_mt(buf.ctypes.data, row0, nrows, cols, seed, tid, ctypes.c_float(scale),
+                                       1 if interleave else 0, os.cpu_count() or 1)
     return torch.from_numpy(buf.view(np.int16)).view(torch.bfloat16)
 
 
@@ -102,37 +104,44 @@ class ModelSpec:
 
 
 class OracleModel:
-    """fp32 CPU restatement of the Qwen2-style prefill forward."""
+    """fp32 CPU restatement of the Qwen2-style prefill forward.
 
-    def __init__(self, spec: ModelSpec, threads: int | None = None):
+    stream=True never holds more than one decoder layer's weights: each
+    forward_seq() call regenerates layer l from the counter RNG, runs layer l
+    of every batch it was given (in order — batch k+1's layer l only needs
+    batch k's layer-l KV), and drops it. That makes full-depth Qwen2.5-32B
+    checks fit in host memory (one fp32 layer = 2 GB instead of 125 GB)."""
+
+    def __init__(self, spec: ModelSpec, threads: int | None = None, stream: bool = False):
         if threads:
             torch.set_num_threads(threads)
         self.s = spec
         s = spec
         scale = float(np.float32(np.float32(s.init_std) * np.float32(math.sqrt(3.0))) / np.float32(8388608.0))
         self.scale = scale
-        seed = s.weight_seed
-        self.layers = []
-        for l in range(s.layers):
-            base = TID_LAYER_BASE + TID_LAYER_STRIDE * l
-            w = {
-                "wqkv": weight_bf16(s.qkv_out, s.hidden, seed, base + T_QKV, scale).float(),
-                "bqkv": weight_bf16(1, s.qkv_out, seed, base + T_QKV_BIAS, scale).float()[0],
-                "wo": weight_bf16(s.hidden, s.n_q_heads * s.head_dim, seed, base + T_O, scale).float(),
-                "wgate": weight_bf16(s.intermediate, s.hidden, seed, base + T_GATE, scale).float(),
-                "wup": weight_bf16(s.intermediate, s.hidden, seed, base + T_UP, scale).float(),
-                "wd": weight_bf16(s.hidden, s.intermediate, seed, base + T_DOWN, scale).float(),
-            }
-            self.layers.append(w)
+        self.stream = stream
+        self.layers = None if stream else [self.layer_weights(l) for l in range(s.layers)]
         emb_scale = float(np.float32(math.sqrt(3.0)) / np.float32(8388608.0))
-        self.embed = weight_bf16(s.vocab, s.hidden, seed, TID_EMBED, emb_scale).float()
-        self.lm_head = weight_bf16(s.vocab, s.hidden, seed, TID_LM_HEAD, scale).float()
+        self.embed = weight_bf16(s.vocab, s.hidden, s.weight_seed, TID_EMBED, emb_scale).float()
+        self.lm_head = weight_bf16(s.vocab, s.hidden, s.weight_seed, TID_LM_HEAD, scale).float()
         d = s.head_dim
         self.inv_freq = torch.tensor(
             [np.float32(1.0 / math.pow(float(np.float32(s.rope_theta)), (2.0 * i) / d)) for i in range(d // 2)],
             dtype=torch.float32)
         # Logical KV per session: list over layers of (K, V) [pos, nkv, d] fp32 (bf16 values).
         self.kv: dict[int, list[list[torch.Tensor]]] = {}
+
+    def layer_weights(self, l: int) -> dict:
+        s, scale, seed = self.s, self.scale, self.s.weight_seed
+        base = TID_LAYER_BASE + TID_LAYER_STRIDE * l
+        return {
+            "wqkv": weight_bf16(s.qkv_out, s.hidden, seed, base + T_QKV, scale).float(),
+            "bqkv": weight_bf16(1, s.qkv_out, seed, base + T_QKV_BIAS, scale).float()[0],
+            "wo": weight_bf16(s.hidden, s.n_q_heads * s.head_dim, seed, base + T_O, scale).float(),
+            "wgate": weight_bf16(s.intermediate, s.hidden, seed, base + T_GATE, scale).float(),
+            "wup": weight_bf16(s.intermediate, s.hidden, seed, base + T_UP, scale).float(),
+            "wd": weight_bf16(s.hidden, s.intermediate, seed, base + T_DOWN, scale).float(),
+        }
 
     # -- building blocks ----------------------------------------------------
     def rmsnorm(self, x: torch.Tensor) -> torch.Tensor:
@@ -186,45 +195,67 @@ class OracleModel:
         """members: (session, new_tokens L, history H) in plan order; toks[i]
         are member i's L new token ids. Returns fp32 logits [n, vocab] of the
         last new token per member; updates the logical KV cache."""
+        return self.forward_seq([(members, toks)])[0]
+
+    def forward_seq(self, batches: list[tuple[list[tuple[int, int, int]], list[np.ndarray]]]) -> list[torch.Tensor]:
+        """Several forwards in submission order, evaluated layer-major (each
+        layer's weights are materialised once for all of them)."""
+        s = self.s
+        states = []
+        for members, toks in batches:
+            ids = torch.from_numpy(np.concatenate(toks).astype(np.int64))
+            x = self.embed[ids].clone()
+            states.append({
+                "members": members, "x": x, "xn": self.rmsnorm(x),
+                "pos": torch.cat([torch.arange(H, H + L) for (_, L, H) in members]),
+                "starts": np.cumsum([0] + [L for (_, L, _) in members]),
+                "checked": False,
+            })
+        for l in range(s.layers):
+            w = self.layer_weights(l) if self.stream else self.layers[l]
+            for st in states:
+                if not st["checked"]:  # history residency, at the batch's turn in submission order
+                    for (sid, L, H) in st["members"]:
+                        if self.kv_len(sid) < H:
+                            raise ValueError(f"session {sid}: history {H} not resident ({self.kv_len(sid)})")
+                    st["checked"] = True
+                self._layer(l, w, st)
+            del w
+        out = []
+        for st in states:
+            last = torch.tensor([st["starts"][i + 1] - 1 for i in range(len(st["members"]))])
+            out.append(st["xn"][last] @ self.lm_head.t())
+        return out
+
+    def _layer(self, l: int, w: dict, st: dict) -> None:
         s = self.s
         nq, nkv, d = s.n_q_heads, s.n_kv_heads, s.head_dim
-        G = nq // nkv
-        for (sid, L, H) in members:
-            if self.kv_len(sid) < H:
-                raise ValueError(f"session {sid}: history {H} not resident ({self.kv_len(sid)})")
-        ids = torch.from_numpy(np.concatenate(toks).astype(np.int64))
-        pos = torch.cat([torch.arange(H, H + L) for (_, L, H) in members])
-        x = self.embed[ids].clone()
+        members, starts, pos, x, xn = st["members"], st["starts"], st["pos"], st["x"], st["xn"]
+        qkv = xn @ w["wqkv"].t() + w["bqkv"]
+        q = qkv[:, : nq * d].view(-1, nq, d)
+        k = qkv[:, nq * d: (nq + nkv) * d].view(-1, nkv, d)
+        v = qkv[:, (nq + nkv) * d:].view(-1, nkv, d)
+        q, k, v = bf16r(self.rope(q, pos)), bf16r(self.rope(k, pos)), bf16r(v)
+        out = torch.empty(q.shape[0], nq * d)
+        for i, (sid, L, H) in enumerate(members):
+            a, b = starts[i], starts[i + 1]
+            cache = self.kv.setdefault(sid, [[torch.zeros(0, nkv, d), torch.zeros(0, nkv, d)]
+                                             for _ in range(s.layers)])
+            K0, V0 = cache[l]
+            K = torch.cat([K0[:H], k[a:b]], 0)
+            V = torch.cat([V0[:H], v[a:b]], 0)
+            if K0.shape[0] > H + L:  # keep resident positions beyond this member
+                K = torch.cat([K, K0[H + L:]], 0)
+                V = torch.cat([V, V0[H + L:]], 0)
+            cache[l] = [K, V]
+            out[a:b] = bf16r(self.attend(q[a:b], K[: H + L], V[: H + L], H))
+        x = x + out @ w["wo"].t()
         xn = self.rmsnorm(x)
-        starts = np.cumsum([0] + [L for (_, L, _) in members])
-        for l, w in enumerate(self.layers):
-            qkv = xn @ w["wqkv"].t() + w["bqkv"]
-            q = qkv[:, : nq * d].view(-1, nq, d)
-            k = qkv[:, nq * d: (nq + nkv) * d].view(-1, nkv, d)
-            v = qkv[:, (nq + nkv) * d:].view(-1, nkv, d)
-            q, k, v = bf16r(self.rope(q, pos)), bf16r(self.rope(k, pos)), bf16r(v)
-            out = torch.empty(q.shape[0], nq * d)
-            for i, (sid, L, H) in enumerate(members):
-                a, b = starts[i], starts[i + 1]
-                cache = self.kv.setdefault(sid, [[torch.zeros(0, nkv, d), torch.zeros(0, nkv, d)]
-                                                 for _ in range(s.layers)])
-                K0, V0 = cache[l]
-                K = torch.cat([K0[:H], k[a:b]], 0)
-                V = torch.cat([V0[:H], v[a:b]], 0)
-                if K0.shape[0] > H + L:  # keep resident positions beyond this member
-                    K = torch.cat([K, K0[H + L:]], 0)
-                    V = torch.cat([V, V0[H + L:]], 0)
-                cache[l] = [K, V]
-                out[a:b] = bf16r(self.attend(q[a:b], K[: H + L], V[: H + L], H))
-            x = x + out @ w["wo"].t()
-            xn = self.rmsnorm(x)
-            g = bf16r(xn @ w["wgate"].t())
-            u = bf16r(xn @ w["wup"].t())
-            act = bf16r(torch.nn.functional.silu(g) * u)
-            x = x + act @ w["wd"].t()
-            xn = self.rmsnorm(x)
-        last = torch.tensor([starts[i + 1] - 1 for i in range(len(members))])
-        return xn[last] @ self.lm_head.t()
+        g = bf16r(xn @ w["wgate"].t())
+        u = bf16r(xn @ w["wup"].t())
+        act = bf16r(torch.nn.functional.silu(g) * u)
+        x = x + act @ w["wd"].t()
+        st["x"], st["xn"] = x, self.rmsnorm(x)
 
     def read_kv(self, session: int, layer: int, pos0: int, n: int):
         K, V = self.kv[session][layer]

@@ -276,7 +276,7 @@ def test_7b_full_depth_against_oracle():
     from paper_2601_11589_b200.instance import QWEN25_7B
     inst = PrefillInstance(QWEN25_7B, max_tokens=1024, max_members=8, kv_pages=64)
     inst.capture_graphs(lengths=(64,), depths=(2,))
-    oracle = FO.OracleModel(FO.QWEN25_7B, threads=os.cpu_count())
+    oracle = FO.OracleModel(FO.QWEN25_7B, threads=os.cpu_count(), stream=True)
     pages = PageOracle(64)
     M = Member
     tol = (0.3, 0.05, 0.999)

@@ -1,0 +1,139 @@
+"""Full-depth parity of the production model shapes against the streaming CPU
+oracle (oracle/forward_oracle.py, stream=True: one layer's weights at a time).
+
+Tolerances (logits; page tables exact): bf16 storage rounding accumulates
+over depth, so at full depth the bound is on direction and mean — cosine
+> 0.999 per member (BASELINE.json), mean-abs <= 0.05 and max-abs <= 0.3 at
+logit std ~1.2 over a 152,064-word vocabulary. Greedy first tokens must agree
+wherever the oracle's top-2 margin exceeds 2 x max-abs.
+
+Batch invariance: the GEMM tile / split-K plan depends on the live token
+count, so a request's logits depend (at the bf16-rounding level) on the batch
+the scheduler put it in. The 7B test measures that directly — the same 16
+requests as one 256x16 graph batch and one by one through 256x1 graphs — and
+bounds it like the oracle gap (cosine > 0.9999, first tokens agree).
+
+Measured numbers are written to $LP_PARITY_OUT (JSON lines) when set
+(profiles/r02_full_depth_parity.jsonl)."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import forward_oracle as FO
+from oracle.pages import PageOracle
+from paper_2601_11589_b200.instance import KIND_GRAPH, KIND_STANDARD, Member, PrefillInstance
+
+pytestmark = pytest.mark.gpu
+SEED = 7
+TOL = (0.3, 0.05, 0.999)  # max-abs, mean-abs, min cosine
+
+
+def _record(name, **kv):
+    path = os.environ.get("LP_PARITY_OUT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"test": name, **kv}) + "\n")
+
+
+def _toks(members, vocab):
+    return [FO.tokens(SEED, m.session_id, m.history, m.new_tokens, vocab) for m in members]
+
+
+def _run(inst, pages, batches):
+    """Submit the batches on the GPU (recording logits / first tokens / page
+    tables) and return what the oracle needs."""
+    got, firsts, seqs = [], [], []
+    for l_pad, depth, kind, members in batches:
+        toks = _toks(members, inst.model.vocab)
+        inst.forward(l_pad, depth, kind, members, np.concatenate(toks))
+        got.append(torch.from_numpy(inst.logits()))
+        firsts.append(inst.next_tokens())
+        pages.submit([(m.session_id, m.new_tokens, m.history) for m in members])
+        for m in members:
+            assert inst.session_pages(m.session_id) == pages.table(m.session_id)
+        seqs.append(([(m.session_id, m.new_tokens, m.history) for m in members], toks))
+    return got, firsts, seqs
+
+
+def _check(name, got, firsts, want):
+    out = []
+    for b, (g, f, w) in enumerate(zip(got, firsts, want)):
+        d = (g - w).abs()
+        cos = torch.nn.functional.cosine_similarity(g, w, dim=1)
+        top2 = torch.topk(w, 2, dim=1).values
+        decisive = (top2[:, 0] - top2[:, 1]) > 2 * TOL[0]
+        agree = [int(f[i]) == int(torch.argmax(w[i])) for i in range(w.shape[0])]
+        rec = {"batch": b, "max_abs": d.max().item(), "mean_abs": d.mean().item(), "min_cos": cos.min().item(),
+               "first_token_agree": sum(agree), "members": len(agree), "logit_std": w.std().item()}
+        _record(name, **rec)
+        out.append(rec)
+        assert rec["max_abs"] <= TOL[0] and rec["mean_abs"] <= TOL[1] and rec["min_cos"] > TOL[2], rec
+        for i in range(w.shape[0]):
+            if decisive[i]:
+                assert agree[i], f"{name} batch {b} member {i}: first token"
+    return out
+
+
+def test_32b_full_depth_against_streaming_oracle():
+    """All 64 layers of the Qwen2.5-32B shape: a graph bucket, a 256-token
+    chunk (chunk graph, tcgen05 attention), a chunk over that history and a
+    graph re-prefill over cached pages."""
+    from paper_2601_11589_b200.instance import QWEN25_32B
+    inst = PrefillInstance(QWEN25_32B, max_tokens=1024, max_members=8, kv_pages=64)
+    inst.capture_graphs(lengths=(64,), depths=(2,))
+    pages = PageOracle(64)
+    M = Member
+    batches = [
+        (64, 2, KIND_GRAPH, [M(0, 0, 50, 0), M(1, 1, 40, 0)]),
+        (256, 1, KIND_STANDARD, [M(2, 2, 256, 0)]),
+        (256, 1, KIND_STANDARD, [M(3, 2, 256, 256)]),
+        (64, 2, KIND_GRAPH, [M(4, 0, 30, 50), M(5, 3, 64, 0)]),
+    ]
+    got, firsts, seqs = _run(inst, pages, batches)
+    inst.close()
+    oracle = FO.OracleModel(FO.QWEN25_32B, threads=os.cpu_count(), stream=True)
+    want = oracle.forward_seq(seqs)
+    _check("32b_full_depth", got, firsts, want)
+
+
+def test_7b_full_depth_bucket_256x16_and_batch_invariance():
+    """All 28 layers of the Qwen2.5-7B shape on the 256x16 graph bucket (16
+    members of 129-256 tokens, ~3K tokens), an H=1024 re-prefill, and the
+    same 16 requests served one by one (batch invariance)."""
+    from paper_2601_11589_b200.instance import QWEN25_7B
+    inst = PrefillInstance(QWEN25_7B, max_tokens=4096, max_members=16, kv_pages=256)
+    inst.capture_graphs(lengths=(64, 256), depths=(1, 16))
+    pages = PageOracle(256)
+    rng = np.random.default_rng(5)
+    M = Member
+    bucket = [M(i, 100 + i, int(rng.integers(129, 257)), 0) for i in range(16)]
+    batches = [
+        (256, 16, KIND_GRAPH, bucket),
+        (512, 1, KIND_STANDARD, [M(20, 200, 512, 0)]),
+        (512, 1, KIND_STANDARD, [M(20, 200, 512, 512)]),
+        (64, 1, KIND_GRAPH, [M(21, 200, 40, 1024)]),
+    ]
+    got, firsts, seqs = _run(inst, pages, batches)
+    # The same 16 requests one at a time (256x1 graph, other split-K plans).
+    alone, alone_first = [], []
+    for m in bucket:
+        inst.release(m.session_id)
+        toks = _toks([m], inst.model.vocab)
+        inst.forward(256, 1, KIND_GRAPH, [m], np.concatenate(toks))
+        alone.append(torch.from_numpy(inst.logits())[0])
+        alone_first.append(int(inst.next_tokens()[0]))
+    inst.close()
+    alone = torch.stack(alone)
+    d = (alone - got[0]).abs()
+    cos = torch.nn.functional.cosine_similarity(alone, got[0], dim=1)
+    agree = sum(int(a == b) for a, b in zip(alone_first, firsts[0]))
+    _record("7b_batch_invariance", max_abs=d.max().item(), mean_abs=d.mean().item(), min_cos=cos.min().item(),
+            first_token_agree=agree, members=16)
+    assert cos.min().item() > 0.9999 and d.mean().item() <= 1e-2
+    assert agree >= 15  # a near-tie may flip; the oracle check below pins decisive ones
+    oracle = FO.OracleModel(FO.QWEN25_7B, threads=os.cpu_count(), stream=True)
+    want = oracle.forward_seq(seqs)
+    _check("7b_full_depth", got, firsts, want)

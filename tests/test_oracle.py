@@ -85,3 +85,17 @@ def test_rope_is_a_rotation(tiny):
     y = tiny.rope(x, pos)
     assert torch.allclose(y.norm(dim=-1), x.norm(dim=-1), rtol=1e-5)
     assert torch.allclose(y[0], x[0])  # position 0 is the identity
+
+
+def test_streaming_oracle_matches_resident_weights():
+    """stream=True (one layer's weights at a time, layer-major over a sequence
+    of forwards) is the same computation as the resident-weight oracle."""
+    import torch
+    a, b = FO.OracleModel(FO.TINY), FO.OracleModel(FO.TINY, stream=True)
+    t1, t2, t3 = (FO.tokens(7, 0, 0, 50, 1024), FO.tokens(7, 0, 50, 20, 1024), FO.tokens(7, 1, 0, 33, 1024))
+    r1 = a.forward([(0, 50, 0), (1, 33, 0)], [t1, t3])
+    r2 = a.forward([(0, 20, 50)], [t2])
+    s1, s2 = b.forward_seq([([(0, 50, 0), (1, 33, 0)], [t1, t3]), ([(0, 20, 50)], [t2])])
+    assert torch.equal(r1, s1) and torch.equal(r2, s2)
+    for l in range(FO.TINY.layers):
+        assert torch.equal(a.read_kv(0, l, 0, 70)[0], b.read_kv(0, l, 0, 70)[0])
