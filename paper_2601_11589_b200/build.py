@@ -30,6 +30,13 @@ CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-I", str(ROOT / 
              "-I", str(CSRC), "-I", str(CSRC / "host")]
 
 
+def _cuda_include() -> str:
+    for cand in ("/usr/local/cuda/include",):
+        if os.path.exists(os.path.join(cand, "nvtx3")):
+            return cand
+    return str(Path(shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc").resolve().parent.parent / "include")
+
+
 def _nvcc() -> str:
     for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
         if cand and os.path.exists(cand):
@@ -57,7 +64,7 @@ def _compile(src: Path, obj: Path, force: bool) -> str:
     if src.suffix == ".cu":
         cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
     else:
-        cmd = [os.environ.get("CXX", "g++"), *CXX_FLAGS, "-c", str(src), "-o", str(obj)]
+        cmd = [os.environ.get("CXX", "g++"), *CXX_FLAGS, "-isystem", _cuda_include(), "-c", str(src), "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

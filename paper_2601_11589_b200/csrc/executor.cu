@@ -9,6 +9,8 @@
 #include "abi_common.h"
 #include "executor.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace lp {
 
 namespace {
@@ -415,7 +417,12 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
   (void)G;
 
   embed_rmsnorm(rc, md_.tokens, embed_, layers_[0].g_attn, x_resid_, x_norm_, st);
+  // NVTX: one range per decoder layer of an eager launch / a capture (host
+  // side; a graph replay shows up as the caller's "lp_submit" range).
+  char layer_tag[32];
   for (int l = 0; l < m_.layers; ++l) {
+    std::snprintf(layer_tag, sizeof layer_tag, "layer %d", l);
+    nvtxRangePushA(layer_tag);
     const LayerW& w = layers_[l];
     bf16* kv_layer = kv_pool_ + layer_stride_ * l;
     // QKV projection -> fp32 split partials.
@@ -474,6 +481,7 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
     gemm(w.tm_d, p.d, g, act_, t_max_, st);
     const bf16* g_next = (l + 1 < m_.layers) ? layers_[l + 1].g_attn : g_final_;
     resid_rmsnorm(rc, ws_, 0, d_fused ? nullptr : md_.scalars + 6, t_cap, x_resid_, g_next, x_norm_, st);
+    nvtxRangePop();
   }
   // Final norm already applied; LM head on the last real token per member.
   gather_rows(n_mem, r_cap, md_.last_idx, x_norm_, x_last_, h, next_keys_, st);
@@ -582,7 +590,13 @@ void Instance::ticket_tokens(int64_t id, int32_t* out, int n) {
   for (int i = 0; i < n; ++i) out[i] = argmax_token(tk.keys[i]);
 }
 
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, const int32_t* tokens) {
+  const NvtxRange range(shape.kind == LP_KIND_GRAPH ? "lp_submit graph" : shape.kind == LP_KIND_PACKED ? "lp_submit packed" : "lp_submit standard");
   lp_check(cudaSetDevice(d_.device), "set device");
   if (n < 1) throw ShapeMismatch("empty batch");
   if (n > r_max_) throw ShapeMismatch("batch of " + std::to_string(n) + " exceeds max_members");

@@ -29,6 +29,8 @@
 #include <sstream>
 #include <unordered_map>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../../include/laps_engine.h"
 #include "laps_host.hpp"
 
@@ -66,7 +68,8 @@ class GpuTier final : public ForwardBackend {
  public:
   GpuTier(lp_instance** insts, int n, int32_t mode, uint64_t token_seed, int32_t vocab,
           const std::vector<Request>& reqs, const lp_sim_opts& opts)
-      : gpus_(insts, insts + n), mode_(mode), seed_(token_seed), vocab_(vocab), opts_(opts), pending_(gpus_.size()) {
+      : gpus_(insts, insts + n), mode_(mode), seed_(token_seed), vocab_(vocab), opts_(opts), pending_(gpus_.size()),
+        next_ticket_(gpus_.size(), 0) {
     for (const Request& r : reqs) turns_[r.session_id] += 1;
   }
 
@@ -85,6 +88,14 @@ class GpuTier final : public ForwardBackend {
                         k < opts_.window_first + opts_.window_count;
     if (opts_.window_count > 0 && !before && !inside && opts_.stop_after_window) return 0;  // clock only
     if (inside && k == opts_.window_first) open_window();
+    char tag[96];  // NVTX: one range per engine dispatch (profilers: --nvtx-include "dispatch*")
+    std::snprintf(tag, sizeof tag, "dispatch %lld lane %d %s %lldx%d", static_cast<long long>(k), call.inst,
+                  call.kind == ForwardKind::kLongChunk ? "chunk" : call.kind == ForwardKind::kPacked ? "packed" : "batch",
+                  static_cast<long long>(call.shape.l_pad), call.shape.depth);
+    nvtxRangePushA(tag);
+    struct Pop {
+      ~Pop() { nvtxRangePop(); }
+    } pop;
     const int g = call.inst % static_cast<int>(gpus_.size());
     for (const ForwardRow& row : call.rows) make_resident(g, row.session_id, row.history, inside);
 
@@ -188,10 +199,15 @@ class GpuTier final : public ForwardBackend {
   size_t submit(Forward f, const lp_shape& shape, const lp_member* m, int32_t n, const int32_t* toks) {
     lp_instance* inst = gpus_[static_cast<size_t>(f.gpu)];
     auto& queue = pending_[static_cast<size_t>(f.gpu)];
-    while (queue.size() >= kAhead) {
+    // Collect by AGE, not by count: forwards the engine polls are harvested
+    // out of order, so a fill could otherwise outlive the instance's ticket
+    // ring. Tickets are issued in order per instance, so the queue (submit
+    // order) has its oldest entry in front.
+    const std::int64_t next = next_ticket_[static_cast<size_t>(f.gpu)];
+    while (!queue.empty() && log_[queue.front()].ticket + static_cast<std::int64_t>(kAhead) <= next)
       harvest(log_[queue.front()]);
-    }
     ok(lp_submit_async(inst, &shape, m, n, toks, &f.ticket), "lp_submit_async");
+    next_ticket_[static_cast<size_t>(f.gpu)] = f.ticket + 1;
     if (f.in_window) {
       int32_t kernels = 0;
       int64_t h2d = 0, d2h = 0;
@@ -338,7 +354,8 @@ class GpuTier final : public ForwardBackend {
   uint64_t seed_;
   int32_t vocab_;
   lp_sim_opts opts_;
-  std::vector<std::vector<size_t>> pending_;  // per GPU: unharvested forwards (log_ indices)
+  std::vector<std::vector<size_t>> pending_;  // per GPU: unharvested forwards (log_ indices, submit order)
+  std::vector<std::int64_t> next_ticket_;      // per GPU: the ticket its next submit will get (known after one)
   std::vector<Forward> log_;
   std::int64_t dispatches_ = 0;
   std::unordered_map<std::int64_t, int> turns_, turns_done_;

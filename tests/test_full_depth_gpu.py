@@ -151,9 +151,14 @@ def test_7b_full_depth_bucket_256x16_and_batch_invariance():
         alone_first.append(int(inst.next_tokens()[0]))
     inst.close()
     floor = _gap(torch.stack(alone), got[0])
-    agree = sum(int(a == b) for a, b in zip(alone_first, firsts[0]))
-    _record("7b_batch_invariance", **floor, first_token_agree=agree, members=16)
-    assert floor["min_cos"] > 0.999 and agree >= 15  # a near-tie may flip; decisive ones are pinned below
+    agree = [int(a == b) for a, b in zip(alone_first, firsts[0])]
+    top2 = torch.topk(got[0], 2, dim=1).values
+    margin = (top2[:, 0] - top2[:, 1]).tolist()
+    _record("7b_batch_invariance", **floor, first_token_agree=sum(agree), members=16,
+            flipped_margins=[m for m, a in zip(margin, agree) if not a])
+    assert floor["min_cos"] > 0.999
+    for m, a in zip(margin, agree):  # a greedy token may flip only inside the noise band
+        assert a or m <= 2 * floor["max_abs"], (m, floor)
     oracle = FO.OracleModel(FO.QWEN25_7B, threads=os.cpu_count(), stream=True)
     want = oracle.forward_seq(seqs)
     recs = _check("7b_full_depth", got, firsts, want, TOL_7B)
