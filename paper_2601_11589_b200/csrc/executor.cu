@@ -74,16 +74,20 @@ constexpr double kTileOverheadCols = 80.0;
 
 // Per-batch (token tiles, split-K) plan. Weight-streaming batches (< 256 live
 // tokens) keep ceil(n/bn) tiles and the wave-quantisation split choice. For
-// tensor-bound batches the unit count m_tiles * n_tiles * splits is chosen so
-// the last wave is nearly full: time ~ waves * (tile width + kTileOverheadCols)
-// * (K-blocks per split + 2), +3% per extra split (fp32 partial round trip). Tile widths
-// are multiples of 16 (the MMA N is a runtime operand).
-// Relative cost of each extra split-K slice in the tile planner (fp32 partial
-// write + reduce). LP_SPLIT_PENALTY overrides it for experiments.
-static double split_penalty() {
+// tensor-bound batches the plan minimises an estimate in microseconds:
+//   waves * (tile width + kTileOverheadCols) * (K-blocks per split + 2) * kUsPerColKb
+//   + (S - 1) * M * n_live * 8 B / partial bandwidth
+// — every extra split writes one more fp32 partial of the output in the GEMM
+// and the reduction kernel (qkv_post / resid_rmsnorm) reads it back. Tile
+// widths are multiples of 16 (the MMA N is a runtime operand). The constants
+// are fitted to the tile sweeps of profiles/r02_tile_sweep.txt (32B QKV at 512
+// tokens: 1 split 32.8 us; the former +3 %-per-split charge chose 5 splits and
+// made the reduction read 73 MB of partials instead of 15).
+constexpr double kUsPerColKb = 1.19e-3;  // one tile column x one 64-deep K block, per CTA (pair)
+static double partial_bytes_per_us() {
   static const double v = [] {
-    const char* e = std::getenv("LP_SPLIT_PENALTY");
-    return e ? std::atof(e) : 0.03;
+    const char* e = std::getenv("LP_PARTIAL_GBS");  // experiments: effective partial bandwidth, GB/s
+    return (e ? std::atof(e) : 4000.0) * 1e3;
   }();
   return v;
 }
@@ -105,7 +109,8 @@ TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms) {
     for (int s = 1; s <= p.s_cap; ++s) {
       const long units = long(m_tiles) * nt * s;
       const double waves = static_cast<double>((units + workers - 1) / workers);
-      const double cost = waves * (tw + kTileOverheadCols) * (double(nk) / s + 2.0) * (1.0 + split_penalty() * (s - 1));
+      const double cost = waves * (tw + kTileOverheadCols) * (double(nk) / s + 2.0) * kUsPerColKb +
+                          double(s - 1) * M * n_live * 8.0 / partial_bytes_per_us();
       if (cost < best * (1 - 1e-9)) {
         best = cost;
         t.n_tiles = nt;
@@ -719,7 +724,14 @@ int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, con
   // only adds a partial round trip and a combine pass.
   // <= 32 splits for the graph path's merge grid; <= 4 for the tcgen05 kernel,
   // whose last split CTA merges the block itself.
-  const int f = std::min(attn_rows == kAttnTcRows ? 4 : 32, std::max(1, target / std::max(ctas, 1)));
+  int f = std::min(attn_rows == kAttnTcRows ? 4 : 32, std::max(1, target / std::max(ctas, 1)));
+  if (attn_rows == kAttnTcRows) {
+    static const int forced = [] {  // experiments: force the tcgen05 key-split factor
+      const char* e = std::getenv("LP_ATTN_TC_SPLIT");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (forced > 0) f = std::min(forced, 4);
+  }
   int nw = 0, nc = 0, n_items = base;
   std::vector<Blk> full;
   for (const Blk& b : blks) {

@@ -390,7 +390,10 @@ void qkv_post(const QkvCtx& c, cudaStream_t st) {
                                                                                  : cap41;
     return threads <= cap;
   };
-  const bool deep = c.s_cap > 2;
+  // Deep split-K only happens below 256 live tokens (the tile planner charges
+  // every extra split its fp32 partial round trip above that), so larger
+  // capacities take the many-CTAs-per-SM <4, 1> variant.
+  const bool deep = c.s_cap > 2 && c.t_cap < 256;
   if (debug_empty("qkv")) return launch_empty(dim3(c.t_cap), dim3(threads_for(deep ? 1 : 4)), st);
   if (deep && fits(reinterpret_cast<const void*>(qkv_post_kernel<1, 8>), threads_for(1))) {
     launch_k(qkv_post_kernel<1, 8>, dim3(c.t_cap), dim3(threads_for(1)), 0, st, c);
