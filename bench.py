@@ -12,8 +12,9 @@ behind the length-aware router (ceil(N/2) short-pool GPUs), all driven by ONE
 host engine (the reference's router is global, sim.cpp:379-411), so
 "scaling": "weak" (per-GPU load fixed).
 
-A step = one dispatched batch forward of the reference scheduler (a graph
-bucket replay or a long-prompt chunk). The engine runs in REPLAY mode: its
+A step = one dispatched batch forward of the reference scheduler per GPU (a
+graph bucket replay or a long-prompt chunk): the window holds K x N dispatches
+at N GPUs, so every GPU runs ~K forwards (weak scaling). The engine runs in REPLAY mode: its
 clock is the reference cost model, so the dispatch sequence is exactly the
 reference scheduler's (deterministic), and every dispatch executes on its GPU
 asynchronously (N GPUs concurrently). Dispatches [0, W) warm up (and build the
@@ -160,8 +161,10 @@ def scenario(n_gpus: int, lam_per_gpu: float, duration_ms: float) -> dict:
     from paper_2601_11589_b200 import scenarios as S
     over = {"workload__lambda_per_ms": lam_per_gpu * n_gpus, "sim__duration_ms": duration_ms}
     if n_gpus > 1:
+        # Spatial pools start at the reference's default split (ceil(N/2) short) and
+        # the Alg. 2 controller moves GPUs between pools (as in config 5).
         over.update(sim__disagg="spatial", sim__instances=n_gpus, sim__initial_short_instances=(n_gpus + 1) // 2,
-                    sim__controller="false")
+                    sim__controller="true" if n_gpus > 2 else "false")
     return S.merged(S.LMSYS_32B, **over)
 
 
@@ -308,7 +311,7 @@ def run_reference(args) -> None:
     ws, rank = dist_env()
     if rank != 0:
         return
-    disp, trace = cost_model_window(args.gpus, args.warmup, args.steps)
+    disp, trace = cost_model_window(args.gpus, args.warmup * args.gpus, args.steps * args.gpus)
     rows = member_rows(disp, trace)
     sampler = CpuSampler()
     # One step = one window dispatch (bounded: ~3 s of CPU work each at most).
@@ -379,10 +382,10 @@ def run_ours(args) -> None:
     barrier(dist)
     with ClockSampler(devices) as clk:
         st = E.simulate(S.text(cfg), "", work / "replay", mode=E.REPLAY, instances=insts, token_seed=TOKEN_SEED,
-                        window=(args.warmup, args.steps), stop_after_window=True)
-    if st.window_dispatches != args.steps:
+                        window=(args.warmup * n, args.steps * n), stop_after_window=True)
+    if st.window_dispatches != args.steps * n:
         raise RuntimeError(f"window ran {st.window_dispatches} dispatches, expected {args.steps}")
-    disp = window_dispatches(work / "replay" / "events.log", args.warmup, args.steps)
+    disp = window_dispatches(work / "replay" / "events.log", args.warmup * n, args.steps * n)
     reqs = request_equivalents(disp)
     value = reqs / (st.window_device_ms / 1000.0)
     e2e_value = reqs / (st.window_wall_ms / 1000.0)
@@ -426,7 +429,8 @@ def run_ours(args) -> None:
         "data": "synthetic (random-init weights from a counter RNG; Poisson LMsys-like multi-turn stream)",
         "config": {"workload": workload_label(n), "model": f"{model_name}-shaped",
                    "parallelism": "1 temporal instance" if n == 1 else f"{n} instances, spatial, one router",
-                   "step": "one dispatch of the reference scheduler (REPLAY clock); requests = request-equivalents "
+                   "step": "one dispatch of the reference scheduler per GPU (window = steps x n_gpus dispatches, "
+                           "REPLAY clock); requests = request-equivalents "
                            "(a chunk of a k-chunk long prompt counts 1/k)",
                    "l2": "no explicit flush: every forward streams the 62 GB of 32B weights (>> 126 MB L2)",
                    "shared_gpu": share},

@@ -136,32 +136,22 @@ __device__ __forceinline__ void merge_block(const AttnCtx& c, int first, int ns,
 // the next launch / graph replay) merges all splits' rows with its warps.
 template <int D>
 __device__ __forceinline__ void attn_merge_if_last(const AttnCtx& c, int wi, int g, int n_warps, int* scratch) {
-  int& s_ci = scratch[0];
   int& s_last = scratch[1];
   __threadfence();
   __syncthreads();
+  const int ci = c.work[wi].x >> 16;  // the block's combine entry (packed by the host)
   if (threadIdx.x == 0) {
-    int ci = 0;
-    const int nc = *c.n_combine;
-    for (int k = 0; k < nc; ++k) {
-      const int4 e = c.combine[k];
-      if (wi >= e.z && wi < e.z + e.w) {
-        ci = k;
-        break;
-      }
-    }
     const int ns = c.combine[ci].w;
     int* cnt = c.comb_cnt + static_cast<size_t>(ci) * c.nkv + g;
     const int old = atomicAdd(cnt, 1);
     const int last = old == ns - 1;
     if (last) *cnt = 0;
-    s_ci = ci;
     s_last = last;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const int4 e = c.combine[s_ci];
+  const int4 e = c.combine[ci];
   (void)n_warps;
   merge_block<D>(c, e.z, e.w, g, e.x, e.y);
 }

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int g = blockIdx.y;
   const int G = c.nq / c.nkv;
   const int4 wk = c.work[wi];
-  const int r = wk.x, row0 = wk.y;
+  const int r = wk.x & 0xFFFF, row0 = wk.y;  // high bits: combine entry of a split item
   const int L = c.q_len[r], H = c.hist[r], qs = c.q_start[r];
   const int rows_total = L * G;
   const int* pages = c.page_list + c.page_off[r];

@@ -152,6 +152,7 @@ Instance::Instance(const lp_model_desc& m, const lp_instance_desc& d) : m_(m), d
   d_.page_size = kPage;
   if (d_.max_tokens <= 0) d_.max_tokens = 16384;
   if (d_.max_members <= 0) d_.max_members = 64;
+  if (d_.max_members > 65535) throw ConfigError("max_members must be <= 65535 (attention work items pack the member index in 16 bits)");
   if (const char* e = std::getenv("LP_FUSE_EPI")) {  // "1" both, "qkv", "resid"
     const std::string v(e);
     fuse_qkv_ = v == "1" || v == "qkv";
@@ -739,7 +740,9 @@ int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, con
     if (s >= 2 && nw + s <= kAttnSplitCap && n_items + s - 1 <= work_cap && nc < combine_cap) {
       mh_.combine[nc++] = make_int4(b.r, b.row0, nw, s);
       for (int k = 0; k < s; ++k)
-        mh_.work[nw++] = make_int4(b.r, b.row0, k * b.need / s, (k + 1) * b.need / s);
+        // .x packs the member (low 16 bits) and this block's combine entry
+        // (high bits): the split CTAs find their merge ticket without a search.
+        mh_.work[nw++] = make_int4(b.r | (nc - 1) << 16, b.row0, k * b.need / s, (k + 1) * b.need / s);
       n_items += s - 1;
     } else {
       full.push_back(b);
