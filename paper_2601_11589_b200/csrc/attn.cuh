@@ -47,12 +47,18 @@ struct AttnCtx {
   float scale_log2;  // log2(e) / sqrt(d)
   int block_rows;    // rows per work item: 64 (warp-MMA kernel) or 128 (tcgen05 kernel)
   int* comb_cnt = nullptr;  // [combine capacity][nkv] split arrival tickets (zero between launches)
+  // Persistent tcgen05 schedule (attn_tc.cu): work[i] = (member, first row,
+  // first page, end page) of piece i, work2[i] = (kv head, combine entry or -1,
+  // partial slot, 0); CTA b runs pieces [cta_off[b], cta_off[b + 1]).
+  const int4* work2 = nullptr;
+  const int* cta_off = nullptr;
 };
 
 constexpr int kAttnRows = 64;    // rows per CTA
 constexpr int kAttnPage = 64;    // required page size (== key tile)
 constexpr int kAttnSplitCap = 1024;  // max split (partial) work items per forward
 constexpr int kAttnTcRows = 128;     // rows per CTA of the tcgen05 kernel (head_dim 128)
+constexpr int kAttnMaxCtas = 256;    // persistent tcgen05 grid: one CTA per SM
 
 // TMA map over the whole paged pool viewed as [planes][64 slots][d] bf16,
 // plane = (layer * n_pages + page) * 2 * nkv + (is_v * nkv + kv_head).
@@ -64,5 +70,8 @@ void attention_prefill(const AttnCtx& c, const CUtensorMap& kv_map, int head_dim
                        int combine_cap, cudaStream_t st, bool with_combine = true);
 // tcgen05/TMEM kernel (head_dim 128, block_rows 128); see attn_tc.cu.
 void attention_prefill_tc(const AttnCtx& c, const CUtensorMap& kv_map, int work_cap, cudaStream_t st);
+// Persistent variant: n_cta CTAs walk the balanced piece lists of the
+// schedule (work / work2 / cta_off), partial pieces merged by the last one.
+void attention_prefill_tc_persistent(const AttnCtx& c, const CUtensorMap& kv_map, int n_cta, cudaStream_t st);
 
 }  // namespace lp

@@ -449,12 +449,409 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (partial) attn_merge_if_last<128>(c, wi, g, kThreads / 32, reinterpret_cast<int*>(smem + TcSmem::kRed));
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent variant. The one-CTA-per-work-item grid leaves SMs idle when the
+// item count is not a multiple of the SM count (7B 512-token chunk: 112 CTAs
+// for 148 SMs; 32B: 160 CTAs = 1.08 waves) and pays the CTA prologue (TMEM
+// allocation, barrier init, pipeline ramp) per item. Here one CTA per SM walks
+// a host-built list of pieces — (128-row block, kv head, page range) — cut
+// so every list costs the same (executor.cu, McNaughton's rule); the TMA
+// rings, S/P buffers and their barrier phases run on one global step counter
+// across pieces (the producer streams the next piece's keys while the current
+// one drains), the Q tile is reloaded per piece once the previous piece's
+// MMAs retired, and a unit split across two lists is merged by its
+// last-finishing piece from fp32 partials.
+constexpr int kPKStages = 3;
+constexpr int kPVStages = 3;
+struct TcpSmem {
+  static constexpr int kQ = 0;                                  // [32 KiB]
+  static constexpr int kK = kQ + kQBytes;                       // [3][32 KiB]
+  static constexpr int kV = kK + kPKStages * kQBytes;           // [3][32 KiB]
+  static constexpr int kBars = kV + kPVStages * kQBytes;
+  static constexpr int kRed = kBars + 256;                      // float [2 parity][2 group][128 rows]
+  static constexpr int kTotal = kRed + 2 * 2 * kRows * 4;       // 231,680 B of the 232,448 B limit
+};
+
+struct Piece {
+  int r, row0, t_begin, t_end, g, ci, slot;
+};
+__device__ __forceinline__ Piece load_piece(const AttnCtx& c, int i) {
+  const int4 a = c.work[i], b = c.work2[i];
+  return Piece{a.x, a.y, a.z, a.w, b.x, b.y, b.z};
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_tcp_kernel(const __grid_constant__ CUtensorMap kvm, const AttnCtx c) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TcpSmem::kBars);
+  uint64_t* k_full = bars + 0;     // [3]
+  uint64_t* k_empty = bars + 3;    // [3]
+  uint64_t* v_full = bars + 6;     // [3]
+  uint64_t* v_empty = bars + 9;    // [3]
+  uint64_t* s_full = bars + 12;    // [2]
+  uint64_t* s_empty = bars + 14;   // [2]
+  uint64_t* p_ready = bars + 16;   // [2]
+  uint64_t* p_free = bars + 18;    // [2]
+  uint64_t* q_ready = bars + 20;   // Q tile of piece j landed (phase j)
+  uint64_t* q_free = bars + 21;    // every MMA of piece j retired (the Q tile may be replaced)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  int* s_flag = reinterpret_cast<int*>(bars + 23);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  pdl_trigger();
+  const int p_beg = c.cta_off[blockIdx.x], p_end = c.cta_off[blockIdx.x + 1];
+  const bool live = p_end > p_beg;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < kPKStages; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < kPVStages; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], kSoftmaxWarps);
+      mbar_init(&p_ready[i], kSoftmaxWarps);
+      mbar_init(&p_free[i], 1);
+    }
+    mbar_init(q_ready, kSoftmaxWarps);
+    mbar_init(q_free, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1 && live) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();
+  if (!live) return;
+  const uint32_t tmem = *tmem_slot;
+  const int G = c.nq / c.nkv;
+  const size_t ld_q = static_cast<size_t>(c.nq) * kD;
+  const uint32_t sQ = smem_u32(smem + TcpSmem::kQ);
+  const uint32_t sK = smem_u32(smem + TcpSmem::kK), sV = smem_u32(smem + TcpSmem::kV);
+  auto steps_of = [](const Piece& p) { return (p.t_end - p.t_begin + 1) / 2; };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producers
+    if (lane < 2) {
+      const bool is_v = lane == 1;
+      uint64_t* full = is_v ? v_full : k_full;
+      uint64_t* empty = is_v ? v_empty : k_empty;
+      uint8_t* ring = smem + (is_v ? TcpSmem::kV : TcpSmem::kK);
+      const int ns = is_v ? kPVStages : kPKStages;
+      int gs = 0;
+      for (int i = p_beg; i < p_end; ++i) {
+        const Piece pc = load_piece(c, i);
+        const int* pages = c.page_list + c.page_off[pc.r];
+        const int n = steps_of(pc);
+        for (int s = 0; s < n; ++s, ++gs) {
+          const int st = gs % ns;
+          mbar_wait(&empty[st], ((gs / ns) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[st], kQBytes);
+          const int t0 = pc.t_begin + 2 * s;
+          const int pg[2] = {pages[t0], t0 + 1 < pc.t_end ? pages[t0 + 1] : pages[t0]};
+#pragma unroll
+          for (int pi = 0; pi < 2; ++pi) {
+            const int plane = c.kv_plane0 + pg[pi] * 2 * c.nkv + pc.g + (is_v ? c.nkv : 0);
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf)
+              tma_load_3d(ring + st * kQBytes + hf * kHalfBytes + pi * 64 * 128, &kvm, &full[st], hf * 64, 0,
+                          plane);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc_s = idesc_bf16(kRows, kKeys);
+    constexpr uint32_t idesc_o = idesc_bf16(kRows, kD) | (1u << 16);  // B (V) is MN-major
+    const uint32_t t_o = tmem + 2 * kKeys;
+    const uint32_t t_p = tmem + 3 * kKeys;
+    int gs = 0;
+    for (int i = p_beg, j = 0; i < p_end; ++i, ++j) {
+      const Piece pc = load_piece(c, i);
+      const int n = steps_of(pc);
+      const uint32_t q_tile = sQ;
+      mbar_wait(q_ready, j & 1);
+      tc_fence_after();
+      auto issue_s = [&](int x) {  // global step x of this piece
+        const int st = x & 1, kst = x % kPKStages;
+        mbar_wait(&k_full[kst], (x / kPKStages) & 1);
+        if (x >= 2) mbar_wait(&s_empty[st], ((x >> 1) & 1) ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < kD / 16; ++k) {
+            const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
+            tc_mma_bf16(tmem + st * kKeys, sdesc_sw128(q_tile + off), sdesc_sw128(sK + kst * kQBytes + off), idesc_s,
+                        k > 0 ? 1u : 0u);
+          }
+          tc_commit(&s_full[st]);
+          tc_commit(&k_empty[kst]);
+        }
+        __syncwarp();
+      };
+      if (n > 0) issue_s(gs);
+      if (n > 1) issue_s(gs + 1);
+      for (int s = 0; s < n; ++s) {
+        const int x = gs + s, st = x & 1, vst = x % kPVStages;
+        mbar_wait(&p_ready[st], (x >> 1) & 1);
+        mbar_wait(&v_full[vst], (x / kPVStages) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < kKeys / 16; ++k) {
+            const uint64_t b = sdesc_sw128_mn(sV + vst * kQBytes + k * 16 * 128, kHalfBytes, 1024);
+            tc_mma_bf16_ts(t_o, t_p + st * 64 + k * 8, b, idesc_o, (s > 0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit(&p_free[st]);
+          tc_commit(&v_empty[vst]);
+        }
+        __syncwarp();
+        if (s + 2 < n) issue_s(x + 2);
+      }
+      if (elect_one()) tc_commit(q_free);  // this piece's MMAs retired: the Q tile may be replaced
+      __syncwarp();
+      gs += n;
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue
+    const int q4 = warp & 3;
+    const int grp = (warp - 2) >> 2;
+    const int rt = q4 * 32 + lane;
+    const int stid = threadIdx.x - 64;         // 0..255 among the softmax threads
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const uint32_t red = smem_u32(smem + TcpSmem::kRed);
+    const int bar_id = 1 + q4;
+    auto pair_sync = [&] { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
+    auto soft_sync = [&] { asm volatile("bar.sync 9, 256;" ::: "memory"); };
+    constexpr int kHalf = kKeys / 2;
+    int gs = 0;
+    for (int i = p_beg, jj = 0; i < p_end; ++i, ++jj) {
+      const Piece pc = load_piece(c, i);
+      const int n = steps_of(pc);
+      const int L = c.q_len[pc.r], H = c.hist[pc.r], qs = c.q_start[pc.r];
+      const int rows_total = L * G;
+      const int row = min(pc.row0 + rt, rows_total - 1);
+      const int j = row / G, hq = pc.g * G + row % G;
+      const int pos = H + j;
+      // Q tile of this piece (the previous piece's MMAs have retired).
+      const uint32_t q_tile = sQ;
+      if (jj >= 1) mbar_wait(q_free, (jj - 1) & 1);
+      const __nv_bfloat16* qrow = c.q + (qs + j) * ld_q + hq * kD;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) cp_async16(tile_addr(q_tile, rt, grp * 8 + ch), qrow + (grp * 8 + ch) * 8);
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_ready);
+
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int s = 0; s < n; ++s) {
+        const int x = gs + s, st = x & 1;
+        mbar_wait(&s_full[st], (x >> 1) & 1);
+        tc_fence_after();
+        float sc[kHalf];
+#pragma unroll
+        for (int cc = 0; cc < kHalf / 16; ++cc)
+          tmem_ld16(tmem + lane_off + st * kKeys + grp * kHalf + cc * 16, sc + cc * 16);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[st]);
+
+        const int kbase = (pc.t_begin + 2 * s) * 64 + grp * kHalf;
+        const int kvalid = min(kKeys, (pc.t_end - pc.t_begin - 2 * s) * 64) - grp * kHalf;
+        float mx = -INFINITY;
+        if (kvalid >= kHalf && kbase + kHalf - 1 <= pos) {
+#pragma unroll
+          for (int k = 0; k < kHalf; ++k) mx = fmaxf(mx, sc[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < kHalf; ++k) {
+            if (k >= kvalid || kbase + k > pos) sc[k] = -INFINITY;
+            mx = fmaxf(mx, sc[k]);
+          }
+        }
+        const uint32_t rb = red + (x & 1) * 2 * kRows * 4;
+        st_shared_f32(rb + (grp * kRows + rt) * 4, mx);
+        pair_sync();
+        mx = fmaxf(mx, ld_shared_f32(rb + ((grp ^ 1) * kRows + rt) * 4));
+        const float m_cand = fmaxf(m_run, mx * c.scale_log2);
+        const bool grow = m_cand > m_run + kRescaleTau || (m_run == -INFINITY && m_cand != -INFINITY);
+        const float m_new = grow ? m_cand : m_run;
+        const float m_use = m_new == -INFINITY ? 0.f : m_new;
+        const float corr = grow ? exp2f(m_run - m_use) : 1.f;
+        m_run = m_new;
+        float sum = 0.f;
+#pragma unroll
+        for (int k = 0; k < kHalf; ++k) {
+          const float xv = sc[k] * c.scale_log2 - m_use;
+          sc[k] = (k % 3 == 2) ? ex2_poly(xv) : ex2_ftz(xv);
+          sum += sc[k];
+        }
+        l_run = l_run * corr + sum;
+        if (x >= 2) {  // P buffer st was read by PV(x - 2)
+          mbar_wait(&p_free[st], ((x >> 1) & 1) ^ 1);
+          tc_fence_after();
+        }
+        if (s > 0 && __any_sync(0xffffffffu, corr != 1.f)) {  // O holds this piece's PVs up to s - 1
+          mbar_wait(&p_free[(x - 1) & 1], ((x - 1) >> 1) & 1);
+          tc_fence_after();
+          const uint32_t t_o = tmem + lane_off + 2 * kKeys + grp * (kD / 2);
+#pragma unroll 1
+          for (int cc = 0; cc < kD / 32; ++cc) {
+            float o[16];
+            tmem_ld16(t_o + cc * 16, o);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) o[q] *= corr;
+            tmem_st16(t_o + cc * 16, o);
+          }
+          tc_wait_st();
+        }
+        {
+          const uint32_t t_pw = tmem + lane_off + 3 * kKeys + st * 64 + grp * 32;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float w[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) w[q] = __uint_as_float(pack_bf16x2(sc[h * 32 + 2 * q], sc[h * 32 + 2 * q + 1]));
+            tmem_st16(t_pw + h * 16, w);
+          }
+          tc_wait_st();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_ready[st]);
+      }
+
+      // Epilogue of the piece: row sum over both column halves, then O / l
+      // (bf16) or the fp32 partial of a split unit.
+      const int xe = gs + n;  // the next step's exchange parity is free of this piece's max exchange
+      const uint32_t lsum = red + (xe & 1) * 2 * kRows * 4;
+      st_shared_f32(lsum + (grp * kRows + rt) * 4, l_run);
+      pair_sync();
+      const float l_tot = l_run + ld_shared_f32(lsum + ((grp ^ 1) * kRows + rt) * 4);
+      pair_sync();  // the next piece's first step writes this parity again
+      if (n > 0) {
+        mbar_wait(&p_free[(xe - 1) & 1], ((xe - 1) >> 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t t_o = tmem + lane_off + 2 * kKeys + grp * (kD / 2);
+      if (pc.ci < 0) {
+        const float inv = 1.f / l_tot;
+        __nv_bfloat16* dst = c.out + (qs + j) * ld_q + hq * kD + grp * (kD / 2);
+#pragma unroll 1
+        for (int cc = 0; cc < kD / 32; ++cc) {
+          float o[16];
+          tmem_ld16(t_o + cc * 16, o);
+          if (pc.row0 + rt < rows_total) {
+            uint4 w[2];
+            uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) wp[q] = pack_bf16x2(o[2 * q] * inv, o[2 * q + 1] * inv);
+            reinterpret_cast<uint4*>(dst + cc * 16)[0] = w[0];
+            reinterpret_cast<uint4*>(dst + cc * 16)[1] = w[1];
+          }
+        }
+        tc_fence_before();
+      } else {
+        float* dst = c.ws_o + (static_cast<size_t>(pc.slot) * kRows + rt) * kD + grp * (kD / 2);
+#pragma unroll 1
+        for (int cc = 0; cc < kD / 32; ++cc) {
+          float o[16];
+          tmem_ld16(t_o + cc * 16, o);
+#pragma unroll
+          for (int q = 0; q < 16; q += 4)
+            *reinterpret_cast<float4*>(dst + cc * 16 + q) = make_float4(o[q], o[q + 1], o[q + 2], o[q + 3]);
+        }
+        tc_fence_before();
+        if (grp == 0) {
+          c.ws_ml[(static_cast<size_t>(pc.slot) * kRows + rt) * 2 + 0] = m_run;
+          c.ws_ml[(static_cast<size_t>(pc.slot) * kRows + rt) * 2 + 1] = l_tot;
+        }
+        // The unit's last piece to finish merges every piece's partial.
+        __threadfence();
+        soft_sync();
+        if (stid == 0) {
+          const int4 e = c.combine[pc.ci];
+          int* cnt = c.comb_cnt + pc.ci;
+          const int last = atomicAdd(cnt, 1) == e.w - 1;
+          if (last) *cnt = 0;
+          *s_flag = last;
+        }
+        soft_sync();
+        if (*s_flag) {
+          __threadfence();
+          const int4 e = c.combine[pc.ci];
+          const int first = e.z, np = e.w;
+          for (int it = stid; it < kRows * (kD / 16); it += 256) {
+            const int rl = it / (kD / 16), qc = it % (kD / 16);
+            const int mrow = pc.row0 + rl;
+            if (mrow >= rows_total) continue;
+            float acc[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[q] = 0.f;
+            float m_all = -INFINITY;
+            for (int k = 0; k < np; ++k)
+              m_all = fmaxf(m_all, __ldcg(c.ws_ml + (static_cast<size_t>(first + k) * kRows + rl) * 2));
+            float l_all = 0.f;
+            for (int k = 0; k < np; ++k) {
+              const size_t sb = static_cast<size_t>(first + k) * kRows + rl;
+              const float mk = __ldcg(c.ws_ml + sb * 2), lk = __ldcg(c.ws_ml + sb * 2 + 1);
+              const float wk = mk == -INFINITY ? 0.f : exp2f(mk - m_all);
+              l_all += wk * lk;
+              const float4* src = reinterpret_cast<const float4*>(c.ws_o + sb * kD + qc * 16);
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                const float4 xv = __ldcg(src + v);
+                acc[4 * v + 0] += wk * xv.x;
+                acc[4 * v + 1] += wk * xv.y;
+                acc[4 * v + 2] += wk * xv.z;
+                acc[4 * v + 3] += wk * xv.w;
+              }
+            }
+            const float inv = 1.f / l_all;
+            const int mj = mrow / G, mh = pc.g * G + mrow % G;
+            __nv_bfloat16* dst = c.out + (qs + mj) * ld_q + mh * kD + qc * 16;
+            uint4 w[2];
+            uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) wp[q] = pack_bf16x2(acc[2 * q] * inv, acc[2 * q + 1] * inv);
+            reinterpret_cast<uint4*>(dst)[0] = w[0];
+            reinterpret_cast<uint4*>(dst)[1] = w[1];
+          }
+        }
+        soft_sync();  // s_flag is rewritten by the next split piece
+      }
+      gs += n;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 }  // namespace
 
 void attention_prefill_tc(const AttnCtx& c, const CUtensorMap& kv_map, int work_cap, cudaStream_t st) {
   constexpr int smem = TcSmem::kTotal;
   smem_attr_once(reinterpret_cast<const void*>(attn_tc_kernel), smem);
   launch_k(attn_tc_kernel, dim3(work_cap, c.nkv), dim3(kThreads), smem, st, kv_map, c);
+}
+
+void attention_prefill_tc_persistent(const AttnCtx& c, const CUtensorMap& kv_map, int n_cta, cudaStream_t st) {
+  constexpr int smem = TcpSmem::kTotal;
+  smem_attr_once(reinterpret_cast<const void*>(attn_tcp_kernel), smem);
+  launch_k(attn_tcp_kernel, dim3(n_cta), dim3(kThreads), smem, st, kv_map, c);
 }
 
 #ifdef LP_ATTN_PROF

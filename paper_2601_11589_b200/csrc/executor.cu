@@ -8,6 +8,7 @@
 
 #include "abi_common.h"
 #include "executor.h"
+#include "launch.cuh"
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -161,6 +162,7 @@ Instance::Instance(const lp_model_desc& m, const lp_instance_desc& d) : m_(m), d
   if (const char* e = std::getenv("LP_GRAPH_ATTN_TC_MIN")) graph_tc_min_ = std::atoi(e);
   if (const char* e = std::getenv("LP_GRAPH_TC_PAIRS")) graph_tc_pairs_ = std::atoll(e);
   if (const char* e = std::getenv("LP_ATTN_TC"); e && e[0] == '0') attn_tc_ = false;
+  if (const char* e = std::getenv("LP_ATTN_PERSIST"); e && e[0] == '0') attn_persist_ = false;
   lp_check(cudaSetDevice(d.device), "cudaSetDevice");
   lp_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   lp_check(cudaEventCreate(&ev_start_), "event");
@@ -262,6 +264,8 @@ void Instance::alloc_arena() {
   r_max_ = d_.max_members;
   c_max_ = (t_max_ * G + kAttnRows - 1) / kAttnRows + r_max_;
   w_max_ = c_max_ + kAttnSplitExtra;
+  // Persistent pieces: every (128-row block, kv head) unit plus one split per CTA boundary.
+  pw_max_ = ((t_max_ * G + kAttnTcRows - 1) / kAttnTcRows + r_max_) * m_.n_kv_heads + 2 * kAttnMaxCtas;
 
   x_resid_ = dmalloc<float>(size_t(t_max_) * h, allocs_);
   x_norm_ = dmalloc<bf16>(size_t(t_max_) * h, allocs_);
@@ -309,8 +313,9 @@ void Instance::alloc_arena() {
   attn_rows_ = (D == 128 && attn_tc_) ? kAttnTcRows : kAttnRows;
   attn_ws_o_ = dmalloc<float>(size_t(kAttnSplitCap) * m_.n_kv_heads * attn_rows_ * D, allocs_);
   attn_ws_ml_ = dmalloc<float>(size_t(kAttnSplitCap) * m_.n_kv_heads * attn_rows_ * 2, allocs_);
-  attn_comb_cnt_ = dmalloc<int>(size_t(c_max_) * m_.n_kv_heads, allocs_);
-  lp_check(cudaMemsetAsync(attn_comb_cnt_, 0, size_t(c_max_) * m_.n_kv_heads * sizeof(int), stream_), "tickets");
+  const size_t n_tickets = size_t(std::max(c_max_, pw_max_)) * m_.n_kv_heads;
+  attn_comb_cnt_ = dmalloc<int>(n_tickets, allocs_);
+  lp_check(cudaMemsetAsync(attn_comb_cnt_, 0, n_tickets * sizeof(int), stream_), "tickets");
   max_pages_ = static_cast<int>(std::min<int64_t>(n_pages_, 4096));
 
   // Metadata block: device + pinned host mirror with identical layout.
@@ -323,8 +328,9 @@ void Instance::alloc_arena() {
   const size_t o_sc = carve(16 * 4), o_tok = carve(size_t(t_max_) * 4), o_pos = carve(size_t(t_max_) * 4),
                o_slot = carve(size_t(t_max_) * 4), o_qs = carve(r_max_ * 4), o_ql = carve(r_max_ * 4),
                o_h = carve(r_max_ * 4), o_li = carve(r_max_ * 4), o_po = carve(r_max_ * 4),
-               o_pt = carve(size_t(r_max_) * max_pages_ * 4), o_w = carve(size_t(w_max_) * 16),
-               o_cb = carve(size_t(c_max_) * 16);
+               o_pt = carve(size_t(r_max_) * max_pages_ * 4), o_w = carve(size_t(std::max(w_max_, pw_max_)) * 16),
+               o_cb = carve(size_t(std::max(c_max_, pw_max_)) * 16), o_w2 = carve(size_t(pw_max_) * 16),
+               o_co = carve(size_t(kAttnMaxCtas + 1) * 4);
   meta_bytes_ = off;
   meta_dev_ = dmalloc<uint8_t>(meta_bytes_, allocs_);
   auto bind = [&](void* base, Meta& m) {
@@ -341,6 +347,8 @@ void Instance::alloc_arena() {
     m.page_off = reinterpret_cast<int*>(b + o_po);
     m.work = reinterpret_cast<int4*>(b + o_w);
     m.combine = reinterpret_cast<int4*>(b + o_cb);
+    m.work2 = reinterpret_cast<int4*>(b + o_w2);
+    m.cta_off = reinterpret_cast<int*>(b + o_co);
   };
   bind(meta_dev_, md_);
   for (Staging& sg : staging_) {
@@ -453,8 +461,11 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
                md_.page_table, md_.page_off, q_, static_cast<int>(int64_t(l) * n_pages_ * 2 * nkv), attn_,
                attn_ws_o_, attn_ws_ml_, nq, nkv,
                static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D))), attn_rows,
-               attn_comb_cnt_};
-    attention_prefill(ac, tm_kv_, D, work_cap, combine_cap, st, combine);
+               attn_comb_cnt_, md_.work2, md_.cta_off};
+    if (attn_rows == kAttnTcRows && attn_persist_ && !debug_empty("attn"))
+      attention_prefill_tc_persistent(ac, tm_kv_, std::min(num_sms(), kAttnMaxCtas), st);
+    else
+      attention_prefill(ac, tm_kv_, D, work_cap, combine_cap, st, combine);
     // O projection + residual + RMSNorm.
     g = GemmArgs{};
     g.M = h; g.N = t_cap; g.K = nq * D; g.n_dev = n_tok; g.ntiles_dev = md_.scalars + 9;
@@ -718,6 +729,126 @@ int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, con
   }
   std::stable_sort(blks.begin(), blks.end(), [](const Blk& a, const Blk& b) { return a.need > b.need; });
   constexpr int kMinSplitTiles = 2;
+  if (attn_rows == kAttnTcRows && attn_persist_) {
+    // Persistent tcgen05 attention: one CTA per SM walks a list of pieces.
+    // A unit = (128-row block, kv head) over the block's causal key range;
+    // units are laid out heaviest first and cut into CTA lists of equal cost
+    // (McNaughton's wrap-around rule, units are divisible along the keys):
+    // every CTA gets ~total/ncta steps, a unit crossing a list boundary is
+    // split into pieces whose fp32 partials the last-finishing piece merges.
+    // Cost model: one step per 128 keys plus kPieceCost steps per piece (Q
+    // tile, pipeline ramp, epilogue).
+    constexpr double kPieceCost = 1.5;
+    const int ncta = std::min(num_sms(), kAttnMaxCtas), nkv = m_.n_kv_heads;
+    const size_t slot_cap = size_t(kAttnSplitCap) * nkv;
+    std::vector<int4> w1, w2;
+    std::vector<int> cta_of;  // CTA of each piece, in creation order
+    int nw = 0, nc = 0;
+    // One walk over the units (heaviest first) at list capacity `cap`;
+    // returns the load of the last list (which takes whatever is left).
+    auto walk = [&](double cap, bool emit) {
+      int cta = 0, slots = 0;
+      double load = 0;
+      nc = 0;
+      for (const Blk& b : blks) {
+        for (int g = 0; g < nkv; ++g) {
+          int p0 = 0, pieces = 0;
+          const int first = static_cast<int>(w1.size());
+          while (p0 < b.need) {
+            const int rem = (b.need - p0 + 1) / 2;  // steps left
+            const double room = cap - load - kPieceCost;
+            const int take = room > 0 ? static_cast<int>(room) : 0;
+            if (cta == ncta - 1 || rem <= room + 0.5) {  // the rest fits (or this is the last list)
+              if (emit) {
+                w1.push_back(make_int4(b.r, b.row0, p0, b.need));
+                cta_of.push_back(cta);
+              }
+              ++pieces;
+              load += rem + kPieceCost;
+              p0 = b.need;
+            } else {
+              if (take >= 1 && rem - take >= 1 && size_t(slots + pieces) + 2 <= slot_cap) {
+                if (emit) {
+                  w1.push_back(make_int4(b.r, b.row0, p0, p0 + 2 * take));
+                  cta_of.push_back(cta);
+                }
+                ++pieces;
+                p0 += 2 * take;
+              }
+              ++cta;
+              load = 0;
+            }
+            if (load >= cap - 1e-9 && cta < ncta - 1) {
+              ++cta;
+              load = 0;
+            }
+          }
+          const int ci = pieces > 1 ? nc++ : -1;
+          if (emit) {
+            if (ci >= 0) mh_.combine[ci] = make_int4(b.r, b.row0 | g << 20, slots, pieces);
+            for (int k = 0; k < pieces; ++k) w2.push_back(make_int4(g, ci, ci >= 0 ? slots + k : 0, 0));
+            (void)first;
+          }
+          if (ci >= 0) slots += pieces;
+        }
+      }
+      return cta == ncta - 1 ? load : 0.0;
+    };
+    // Smallest list capacity whose walk does not overload the last list.
+    double total = 0, biggest = 0;
+    for (const Blk& b : blks) {
+      total += nkv * ((b.need + 1) / 2 + kPieceCost);
+      biggest = std::max(biggest, (b.need + 1) / 2 + kPieceCost);
+    }
+    double lo = total / ncta, hi = lo + 2 * biggest;
+    for (int it = 0; it < 24 && hi - lo > 0.25; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (walk(mid, false) <= mid + 0.5) hi = mid;
+      else lo = mid;
+    }
+    // Whole units, longest first onto the least-loaded list (no splits, no
+    // merges): the schedule to beat. A split schedule pays more than the
+    // nominal kPieceCost per extra piece (merge, fp32 partials, a cold
+    // pipeline): take it only when it wins by 15 % + 6 steps (measured, 7B /
+    // 32B chunks at H = 0..16 K: profiles/r02_attn_experiments.md).
+    std::vector<double> lpt(static_cast<size_t>(ncta), 0.0);
+    std::vector<int> lpt_of;
+    for (const Blk& b : blks) {
+      for (int g = 0; g < nkv; ++g) {
+        const size_t c = static_cast<size_t>(std::min_element(lpt.begin(), lpt.end()) - lpt.begin());
+        lpt[c] += (b.need + 1) / 2 + kPieceCost;
+        lpt_of.push_back(static_cast<int>(c));
+      }
+    }
+    const double lpt_span = *std::max_element(lpt.begin(), lpt.end());
+    if (1.15 * hi + 6.0 < lpt_span) {
+      walk(hi, true);
+    } else {
+      size_t u = 0;
+      nc = 0;
+      for (const Blk& b : blks) {
+        for (int g = 0; g < nkv; ++g, ++u) {
+          w1.push_back(make_int4(b.r, b.row0, 0, b.need));
+          w2.push_back(make_int4(g, -1, 0, 0));
+          cta_of.push_back(lpt_of[u]);
+        }
+      }
+    }
+    if (static_cast<int>(w1.size()) > pw_max_) throw ShapeMismatch("attention schedule exceeds its piece capacity");
+    // Counting sort of the pieces by CTA (stable: a CTA keeps creation order).
+    std::vector<int> count(kAttnMaxCtas + 1, 0);
+    for (int c : cta_of) ++count[static_cast<size_t>(c) + 1];
+    for (int c = 0; c < kAttnMaxCtas; ++c) count[static_cast<size_t>(c) + 1] += count[static_cast<size_t>(c)];
+    for (int c = 0; c <= kAttnMaxCtas; ++c) mh_.cta_off[c] = count[static_cast<size_t>(c)];
+    for (size_t i = 0; i < w1.size(); ++i) {
+      const int at = count[static_cast<size_t>(cta_of[i])]++;
+      mh_.work[at] = w1[i];
+      mh_.work2[at] = w2[i];
+    }
+    nw = static_cast<int>(w1.size());
+    mh_.scalars[2] = nw;
+    mh_.scalars[3] = nc;
+  } else {
   const int base = static_cast<int>(blks.size());
   // One wave for the tcgen05 kernel (one CTA per SM), two for the warp-MMA one.
   const int ctas = base * m_.n_kv_heads, target = (attn_rows == kAttnTcRows ? 1 : 2) * num_sms();
@@ -749,10 +880,12 @@ int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, con
     }
   }
   for (const Blk& b : full) mh_.work[nw++] = make_int4(b.r, b.row0, 0, -1);
-  mh_.scalars[0] = t;
-  mh_.scalars[1] = n;
   mh_.scalars[2] = nw;
   mh_.scalars[3] = nc;
+  }
+  mh_.scalars[0] = t;
+  mh_.scalars[1] = n;
+  const int nw = mh_.scalars[2], nc = mh_.scalars[3];
   // Split-K per projection for the live token count (fused epilogues need 1).
   {
     const SplitPlan sp = plan_for(t_cap, r_cap);
@@ -792,6 +925,10 @@ int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, con
   h2d(md_.page_table, mh_.page_table, size_t(np) * 4);
   h2d(md_.work, mh_.work, size_t(nw) * 16);
   h2d(md_.combine, mh_.combine, size_t(nc) * 16);
+  if (attn_rows == kAttnTcRows && attn_persist_) {
+    h2d(md_.work2, mh_.work2, size_t(nw) * 16);
+    h2d(md_.cta_off, mh_.cta_off, size_t(kAttnMaxCtas + 1) * 4);
+  }
 
   lp_check(cudaEventRecord(staging_[(stage_seq_ - 1) % kStaging].h2d, stream_), "event");
   lp_check(cudaEventRecord(tk.start, stream_), "event");

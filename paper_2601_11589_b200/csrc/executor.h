@@ -53,6 +53,8 @@ struct Meta {
   int* page_off;    // [R] offset of member r in page_table
   int4* work;       // [W] attention work items (see attn.cuh)
   int4* combine;    // [C] split row blocks to merge
+  int4* work2;      // [W] persistent attention pieces: (kv head, combine entry, partial slot, 0)
+  int* cta_off;     // [kAttnMaxCtas + 1] persistent attention: first piece of each CTA
 };
 
 // Launch plan of one projection at a given token capacity.
@@ -199,6 +201,12 @@ class Instance {
   // LP_ATTN_TC=0 selects the warp-MMA kernel (64-row items) instead.
   bool attn_tc_ = true;
   int attn_rows_ = kAttnRows;
+  // The tcgen05 attention runs as a persistent grid (one CTA per SM) over a
+  // balanced piece schedule built per batch (LP_ATTN_PERSIST=0: one CTA per
+  // work item, the round-1 launch).
+  bool attn_persist_ = true;
+  int pw_max_ = 0;  // persistent pieces capacity
+  int plan_persistent_attention(int n, int G);
 
   // graphs
   std::map<int64_t, cudaGraphExec_t> graphs_;
