@@ -36,6 +36,11 @@ int lpk_gemm(const void* W, const void* X, void* out, float* ws, const void* bia
 int lpk_time_gemm(lp_instance* inst, int32_t layer, int32_t which, int32_t t_cap, int32_t n_live,
                   int32_t iters, double* avg_ms);
 
+/* Attention schedule of the last submit: *pieces work pieces (persistent
+ * tcgen05 grid) or work items, *merges units split across CTAs (merged by
+ * their last piece), *ctas CTAs with work. */
+int lpk_last_attention_schedule(lp_instance* inst, int32_t* pieces, int32_t* merges, int32_t* ctas);
+
 /* bf16 bits of weight element `index` of tensor `tensor_id` from the device
  * initialiser's generator (host side; the oracle must reproduce them). */
 uint16_t lpk_synth_weight_bits(uint64_t seed, uint64_t tensor_id, uint64_t index, float scale);

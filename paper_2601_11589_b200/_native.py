@@ -117,5 +117,6 @@ def _declare(L: ctypes.CDLL) -> None:
     sig("lp_last_launches", c_i32, vp, ctypes.POINTER(c_i32))
     sig("lp_timer_elapsed", c_i32, vp, c_i32, c_i32, ctypes.POINTER(c_f64))
     sig("lpk_time_gemm", c_i32, vp, c_i32, c_i32, c_i32, c_i32, c_i32, ctypes.POINTER(c_f64))
+    sig("lpk_last_attention_schedule", c_i32, vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), ctypes.POINTER(c_i32))
     # kernel-level test hooks (include/laps_prefill_testing.h)
     sig("lpk_gemm", c_i32, vp, vp, vp, vp, vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, vp, vp, c_i32)

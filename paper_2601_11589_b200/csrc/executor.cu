@@ -886,6 +886,11 @@ int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, con
   mh_.scalars[0] = t;
   mh_.scalars[1] = n;
   const int nw = mh_.scalars[2], nc = mh_.scalars[3];
+  last_attn_pieces_ = nw;
+  last_attn_merges_ = nc;
+  last_attn_ctas_ = 0;
+  if (attn_rows == kAttnTcRows && attn_persist_)
+    for (int c = 0; c < kAttnMaxCtas; ++c) last_attn_ctas_ += mh_.cta_off[c + 1] > mh_.cta_off[c] ? 1 : 0;
   // Split-K per projection for the live token count (fused epilogues need 1).
   {
     const SplitPlan sp = plan_for(t_cap, r_cap);
@@ -1285,6 +1290,15 @@ int lp_timer_elapsed(lp_instance* inst, int32_t slot_a, int32_t slot_b, double* 
   return lp::lp_guard([&] {
     if (!ms) throw lp::ConfigError("null argument");
     *ms = impl_of(inst).timer_elapsed(slot_a, slot_b);
+  });
+}
+
+int lpk_last_attention_schedule(lp_instance* inst, int32_t* pieces, int32_t* merges, int32_t* ctas) {
+  return lp::lp_guard([&] {
+    Instance& in = impl_of(inst);
+    if (pieces) *pieces = in.last_attn_pieces_;
+    if (merges) *merges = in.last_attn_merges_;
+    if (ctas) *ctas = in.last_attn_ctas_;
   });
 }
 

@@ -231,6 +231,7 @@ class Instance {
  public:
   size_t last_h2d_bytes_ = 0, last_d2h_bytes_ = 0;  // host<->device bytes of the last submit / read
   int last_launches_ = 0;                             // kernels of the last submit
+  int last_attn_pieces_ = 0, last_attn_merges_ = 0, last_attn_ctas_ = 0;  // attention schedule of the last submit
 };
 
 }  // namespace lp

@@ -232,6 +232,13 @@ class PrefillInstance:
         _check(N.lib().lpk_time_gemm(self._h, layer, which, t_cap, n_live, iters, ctypes.byref(ms)))
         return ms.value
 
+    def attention_schedule(self) -> tuple[int, int, int]:
+        """(pieces, split units merged in-kernel, CTAs with work) of the last
+        submit's tcgen05 attention (test hook, laps_prefill_testing.h)."""
+        a, b, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(N.lib().lpk_last_attention_schedule(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
     @staticmethod
     def migrate(src: "PrefillInstance", dst: "PrefillInstance", session_id: int) -> None:
         _check(N.lib().lp_session_migrate(src._h, dst._h, session_id))
