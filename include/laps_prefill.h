@@ -94,7 +94,10 @@ typedef struct lp_member {
   int64_t session_id;
   int64_t new_tokens;   /* L (or chunk length) */
   int64_t history;      /* H (+ preceding chunk tokens for long chunks) */
-  int32_t want_logits;  /* produce first-token output for this member */
+  int32_t want_logits;  /* produce first-token output for this member; when no
+                           member of a forward sets it (an intermediate chunk
+                           of a long prompt, a history fill) the LM head is
+                           skipped and its first tokens read back as -1 */
   int32_t reserved;
 } lp_member;
 

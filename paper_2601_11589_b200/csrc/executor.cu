@@ -500,13 +500,16 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
     resid_rmsnorm(rc, ws_, 0, d_fused ? nullptr : md_.scalars + 6, t_cap, x_resid_, g_next, x_norm_, st);
     nvtxRangePop();
   }
-  // Final norm already applied; LM head on the last real token per member.
-  gather_rows(n_mem, r_cap, md_.last_idx, x_norm_, x_last_, h, next_keys_, st);
+  // Final norm already applied; LM head on the last real token per member —
+  // skipped (0 live rows) when no member wants its first token (an
+  // intermediate long-prompt chunk, a history fill).
+  const int* n_head = md_.scalars + 12;
+  gather_rows(n_head, r_cap, md_.last_idx, x_norm_, x_last_, h, next_keys_, st);
   GemmArgs g;
-  g.M = m_.vocab; g.N = r_cap; g.K = h; g.n_dev = n_mem;
+  g.M = m_.vocab; g.N = r_cap; g.K = h; g.n_dev = n_head;
   g.mode = kEpiF32; g.out = logits_; g.ldo = m_.vocab;
   gemm(tm_lm_, p.lm, g, x_last_, std::max(r_max_, 256), st);
-  argmax_rows(n_mem, r_cap, logits_, m_.vocab, next_keys_, st);
+  argmax_rows(n_head, r_cap, logits_, m_.vocab, next_keys_, st);
 }
 
 std::vector<int32_t> Instance::alloc_pages(int n) {
@@ -538,7 +541,8 @@ void Instance::capture_graphs(const std::vector<int64_t>& lens, const std::vecto
   // Warm the launch paths (function attributes, tensor-map cache) eagerly.
   Meta& mh = acquire_staging();
   mh.scalars[0] = mh.scalars[1] = mh.scalars[2] = mh.scalars[3] = 0;
-  lp_check(cudaMemcpyAsync(md_.scalars, mh.scalars, 16, cudaMemcpyHostToDevice, stream_), "meta");
+  mh.scalars[12] = 0;
+  lp_check(cudaMemcpyAsync(md_.scalars, mh.scalars, 64, cudaMemcpyHostToDevice, stream_), "meta");
   lp_check(cudaEventRecord(staging_[(stage_seq_ - 1) % kStaging].h2d, stream_), "event");
   for (int64_t L : lens) {
     for (int32_t dep : depths) {
@@ -604,7 +608,7 @@ void Instance::ticket_tokens(int64_t id, int32_t* out, int n) {
   Ticket& tk = ticket(id);
   if (n > tk.n) throw ShapeMismatch("asked for more tokens than members");
   lp_check(cudaEventSynchronize(tk.done), "first tokens");
-  for (int i = 0; i < n; ++i) out[i] = argmax_token(tk.keys[i]);
+  for (int i = 0; i < n; ++i) out[i] = tk.logits ? argmax_token(tk.keys[i]) : -1;
 }
 
 struct NvtxRange {
@@ -885,6 +889,9 @@ int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, con
   }
   mh_.scalars[0] = t;
   mh_.scalars[1] = n;
+  bool any_logits = false;
+  for (int i = 0; i < n; ++i) any_logits = any_logits || mem[i].want_logits != 0;
+  mh_.scalars[12] = any_logits ? n : 0;  // LM-head rows
   const int nw = mh_.scalars[2], nc = mh_.scalars[3];
   last_attn_pieces_ = nw;
   last_attn_merges_ = nc;
@@ -918,7 +925,7 @@ int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, con
     if (bytes) lp_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_), "meta h2d");
     last_h2d_bytes_ += bytes;
   };
-  h2d(md_.scalars, mh_.scalars, 48);
+  h2d(md_.scalars, mh_.scalars, 64);
   h2d(md_.tokens, mh_.tokens, size_t(t) * 4);
   h2d(md_.positions, mh_.positions, size_t(t) * 4);
   h2d(md_.slots, mh_.slots, size_t(t) * 4);
@@ -964,6 +971,7 @@ int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, con
   last_d2h_bytes_ = size_t(n) * sizeof(unsigned long long);
   tk.id = id;
   tk.n = n;
+  tk.logits = any_logits;
   ++next_ticket_;
   for (int i = 0; i < n; ++i) {
     Session& s = sessions_[mem[i].session_id];

@@ -140,6 +140,7 @@ class Instance {
   struct Ticket {
     int64_t id = -1;
     int n = 0;
+    bool logits = true;  // the forward ran the LM head (some member wanted its first token)
     cudaEvent_t start = nullptr, end = nullptr, done = nullptr;
     unsigned long long* keys = nullptr;  // pinned [r_max]
   };

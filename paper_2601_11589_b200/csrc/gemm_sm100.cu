@@ -74,6 +74,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // n_dev is written by the pre-graph H2D copy, never by a kernel: safe before pdl_wait.
   const int n_live = args.n_dev ? min(*args.n_dev, args.N) : args.N;
+  if (n_live <= 0) {  // nothing live (e.g. an LM head no member wants): no loads, no MMAs
+    pdl_wait();
+    return;
+  }
   const int m_tiles = args.M / (kBM * kPair);   // tiles of this variant (128 or 256 rows)
   // Token tiles are sized from the LIVE token count: ceil(n_live / BN) tiles
   // of equal width tw (a multiple of 16 <= BN), and each tile's MMA runs with

@@ -105,7 +105,9 @@ class GpuTier final : public ForwardBackend {
     f.gpu = g;
     f.in_window = inside;
     for (const ForwardRow& row : call.rows) {
-      members.push_back(lp_member{row.req_id, row.session_id, row.new_tokens, row.history, 1, 0});
+      // Only a request's final forward needs the LM head (its first token).
+      members.push_back(lp_member{row.req_id, row.session_id, row.new_tokens, row.history,
+                                  row.finishes_request ? 1 : 0, 0});
       for (Tokens p = row.history; p < row.history + row.new_tokens; ++p)
         toks.push_back(lp_synth_token(seed_, row.session_id, p, vocab_));
       f.tokens += row.new_tokens;
