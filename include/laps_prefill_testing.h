@@ -41,6 +41,15 @@ int lpk_time_gemm(lp_instance* inst, int32_t layer, int32_t which, int32_t t_cap
  * their last piece), *ctas CTAs with work. */
 int lpk_last_attention_schedule(lp_instance* inst, int32_t* pieces, int32_t* merges, int32_t* ctas);
 
+/* The persistent attention's planner on the host alone (no GPU): blocks of
+ * `needs[i]` pages (heaviest first) x nkv kv heads onto ncta lists. out
+ * (capacity `cap` pieces) receives per piece {cta, block, kv head, first page,
+ * end page, merge entry or -1}; *lpt_span = -1 when the split lists were
+ * chosen, else the whole-unit makespan; *list_cap = the McNaughton capacity
+ * (steps). */
+int lpk_plan_attention(const int32_t* needs, int32_t n_blocks, int32_t nkv, int32_t ncta, int32_t* out,
+                       int32_t cap, int32_t* n_pieces, int32_t* n_merges, double* list_cap, double* lpt_span);
+
 /* bf16 bits of weight element `index` of tensor `tensor_id` from the device
  * initialiser's generator (host side; the oracle must reproduce them). */
 uint16_t lpk_synth_weight_bits(uint64_t seed, uint64_t tensor_id, uint64_t index, float scale);

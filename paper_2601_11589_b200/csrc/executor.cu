@@ -8,6 +8,7 @@
 
 #include "abi_common.h"
 #include "executor.h"
+#include "attn_plan.h"
 #include "launch.cuh"
 
 #include <nvtx3/nvToolsExt.h>
@@ -734,109 +735,24 @@ int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, con
   std::stable_sort(blks.begin(), blks.end(), [](const Blk& a, const Blk& b) { return a.need > b.need; });
   constexpr int kMinSplitTiles = 2;
   if (attn_rows == kAttnTcRows && attn_persist_) {
-    // Persistent tcgen05 attention: one CTA per SM walks a list of pieces.
-    // A unit = (128-row block, kv head) over the block's causal key range;
-    // units are laid out heaviest first and cut into CTA lists of equal cost
-    // (McNaughton's wrap-around rule, units are divisible along the keys):
-    // every CTA gets ~total/ncta steps, a unit crossing a list boundary is
-    // split into pieces whose fp32 partials the last-finishing piece merges.
-    // Cost model: one step per 128 keys plus kPieceCost steps per piece (Q
-    // tile, pipeline ramp, epilogue).
-    constexpr double kPieceCost = 1.5;
+    // Persistent tcgen05 attention: balanced piece lists (attn_plan.h).
     const int ncta = std::min(num_sms(), kAttnMaxCtas), nkv = m_.n_kv_heads;
-    const size_t slot_cap = size_t(kAttnSplitCap) * nkv;
+    std::vector<AttnBlock> ab;
+    ab.reserve(blks.size());
+    for (const Blk& b : blks) ab.push_back(AttnBlock{b.r, b.row0, b.need});
+    const AttnSchedule sched = plan_attention(ab, nkv, ncta, size_t(kAttnSplitCap) * nkv);
     std::vector<int4> w1, w2;
-    std::vector<int> cta_of;  // CTA of each piece, in creation order
-    int nw = 0, nc = 0;
-    // One walk over the units (heaviest first) at list capacity `cap`;
-    // returns the load of the last list (which takes whatever is left).
-    auto walk = [&](double cap, bool emit) {
-      int cta = 0, slots = 0;
-      double load = 0;
-      nc = 0;
-      for (const Blk& b : blks) {
-        for (int g = 0; g < nkv; ++g) {
-          int p0 = 0, pieces = 0;
-          const int first = static_cast<int>(w1.size());
-          while (p0 < b.need) {
-            const int rem = (b.need - p0 + 1) / 2;  // steps left
-            const double room = cap - load - kPieceCost;
-            const int take = room > 0 ? static_cast<int>(room) : 0;
-            if (cta == ncta - 1 || rem <= room + 0.5) {  // the rest fits (or this is the last list)
-              if (emit) {
-                w1.push_back(make_int4(b.r, b.row0, p0, b.need));
-                cta_of.push_back(cta);
-              }
-              ++pieces;
-              load += rem + kPieceCost;
-              p0 = b.need;
-            } else {
-              if (take >= 1 && rem - take >= 1 && size_t(slots + pieces) + 2 <= slot_cap) {
-                if (emit) {
-                  w1.push_back(make_int4(b.r, b.row0, p0, p0 + 2 * take));
-                  cta_of.push_back(cta);
-                }
-                ++pieces;
-                p0 += 2 * take;
-              }
-              ++cta;
-              load = 0;
-            }
-            if (load >= cap - 1e-9 && cta < ncta - 1) {
-              ++cta;
-              load = 0;
-            }
-          }
-          const int ci = pieces > 1 ? nc++ : -1;
-          if (emit) {
-            if (ci >= 0) mh_.combine[ci] = make_int4(b.r, b.row0 | g << 20, slots, pieces);
-            for (int k = 0; k < pieces; ++k) w2.push_back(make_int4(g, ci, ci >= 0 ? slots + k : 0, 0));
-            (void)first;
-          }
-          if (ci >= 0) slots += pieces;
-        }
-      }
-      return cta == ncta - 1 ? load : 0.0;
-    };
-    // Smallest list capacity whose walk does not overload the last list.
-    double total = 0, biggest = 0;
-    for (const Blk& b : blks) {
-      total += nkv * ((b.need + 1) / 2 + kPieceCost);
-      biggest = std::max(biggest, (b.need + 1) / 2 + kPieceCost);
+    std::vector<int> cta_of;
+    for (const AttnPiece& pc : sched.pieces) {
+      w1.push_back(make_int4(pc.r, pc.row0, pc.t_begin, pc.t_end));
+      w2.push_back(make_int4(pc.g, pc.ci, pc.slot, 0));
+      cta_of.push_back(pc.cta);
     }
-    double lo = total / ncta, hi = lo + 2 * biggest;
-    for (int it = 0; it < 24 && hi - lo > 0.25; ++it) {
-      const double mid = 0.5 * (lo + hi);
-      if (walk(mid, false) <= mid + 0.5) hi = mid;
-      else lo = mid;
-    }
-    // Whole units, longest first onto the least-loaded list (no splits, no
-    // merges): the schedule to beat. A split schedule pays more than the
-    // nominal kPieceCost per extra piece (merge, fp32 partials, a cold
-    // pipeline): take it only when it wins by 15 % + 6 steps (measured, 7B /
-    // 32B chunks at H = 0..16 K: profiles/r02_attn_experiments.md).
-    std::vector<double> lpt(static_cast<size_t>(ncta), 0.0);
-    std::vector<int> lpt_of;
-    for (const Blk& b : blks) {
-      for (int g = 0; g < nkv; ++g) {
-        const size_t c = static_cast<size_t>(std::min_element(lpt.begin(), lpt.end()) - lpt.begin());
-        lpt[c] += (b.need + 1) / 2 + kPieceCost;
-        lpt_of.push_back(static_cast<int>(c));
-      }
-    }
-    const double lpt_span = *std::max_element(lpt.begin(), lpt.end());
-    if (1.15 * hi + 6.0 < lpt_span) {
-      walk(hi, true);
-    } else {
-      size_t u = 0;
-      nc = 0;
-      for (const Blk& b : blks) {
-        for (int g = 0; g < nkv; ++g, ++u) {
-          w1.push_back(make_int4(b.r, b.row0, 0, b.need));
-          w2.push_back(make_int4(g, -1, 0, 0));
-          cta_of.push_back(lpt_of[u]);
-        }
-      }
+    int nw = 0;
+    const int nc = static_cast<int>(sched.merges.size());
+    for (int k = 0; k < nc; ++k) {
+      const AttnMerge& m = sched.merges[static_cast<size_t>(k)];
+      mh_.combine[k] = make_int4(m.r, m.row0 | m.g << 20, m.first_slot, m.n_pieces);
     }
     if (static_cast<int>(w1.size()) > pw_max_) throw ShapeMismatch("attention schedule exceeds its piece capacity");
     // Counting sort of the pieces by CTA (stable: a CTA keeps creation order).
