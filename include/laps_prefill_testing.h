@@ -41,6 +41,13 @@ int lpk_time_gemm(lp_instance* inst, int32_t layer, int32_t which, int32_t t_cap
  * their last piece), *ctas CTAs with work. */
 int lpk_last_attention_schedule(lp_instance* inst, int32_t* pieces, int32_t* merges, int32_t* ctas);
 
+/* The GEMM launch planner on the host alone (no GPU): the capacity plan of a
+ * projection [M out, K in] at t_cap tokens (token tile bn, CTA pair) and the
+ * per-batch (token tiles, split-K) choice for n_live live tokens on `sms` SMs
+ * (allow_split = 0: fused epilogues, one K slice). */
+int lpk_plan_gemm(int32_t M, int32_t K, int32_t t_cap, int32_t n_live, int32_t sms, int32_t allow_split,
+                  int32_t* bn, int32_t* pair, int32_t* n_tiles, int32_t* splits);
+
 /* The persistent attention's planner on the host alone (no GPU): blocks of
  * `needs[i]` pages (heaviest first) x nkv kv heads onto ncta lists. out
  * (capacity `cap` pieces) receives per piece {cta, block, kv head, first page,

@@ -388,6 +388,10 @@ int Instance::work_cap_for(int t_cap, int r_cap) const {
   return std::min(w_max_, block_cap_for(t_cap, r_cap) + extra);
 }
 
+GemmPlan plan_gemm_for_tests(int M, int K, int t_cap, bool allow_split, int sms) {
+  return plan_gemm(M, K, t_cap, allow_split, sms);
+}
+
 SplitPlan Instance::plan_for(int t_cap, int r_cap) const {
   const int sms = num_sms();
   const int h = m_.hidden, D = m_.head_dim;
@@ -1214,6 +1218,21 @@ int lp_timer_elapsed(lp_instance* inst, int32_t slot_a, int32_t slot_b, double* 
   return lp::lp_guard([&] {
     if (!ms) throw lp::ConfigError("null argument");
     *ms = impl_of(inst).timer_elapsed(slot_a, slot_b);
+  });
+}
+
+int lpk_plan_gemm(int32_t M, int32_t K, int32_t t_cap, int32_t n_live, int32_t sms, int32_t allow_split,
+                  int32_t* bn, int32_t* pair, int32_t* n_tiles, int32_t* splits) {
+  return lp::lp_guard([&] {
+    if (M < 128 || K < 64 || t_cap < 1 || n_live < 0 || n_live > t_cap || sms < 2) throw lp::ConfigError("bad arguments");
+    const lp::GemmPlan p = lp::plan_gemm_for_tests(M, K, t_cap, allow_split != 0, sms);
+    lp::GemmPlan q = p;
+    if (!allow_split) q.s_cap = 1;
+    const lp::TilePlan t = lp::choose_tiles(M, K, q, std::max(1, n_live), sms);
+    if (bn) *bn = p.bn;
+    if (pair) *pair = p.pair;
+    if (n_tiles) *n_tiles = t.n_tiles;
+    if (splits) *splits = t.splits;
   });
 }
 

@@ -70,6 +70,7 @@ struct TilePlan {
   int n_tiles = 1, splits = 1;
 };
 TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms);
+GemmPlan plan_gemm_for_tests(int M, int K, int t_cap, bool allow_split, int sms);  // lpk_plan_gemm
 struct SplitPlan {
   GemmPlan qkv, o, gu, d, lm;
 };
