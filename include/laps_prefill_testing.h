@@ -30,6 +30,15 @@ extern "C" {
 int lpk_gemm(const void* W, const void* X, void* out, float* ws, const void* bias, int M, int N, int K,
              int splits, int mode, int bn, int ldo, const int* n_dev, void* stream, int pair);
 
+/* Stream-K launch of the same GEMM (fp32 partial output): the grid's CTAs
+ * (pairs), at most max_ctas CTAs (0 = one per SM), split the (tile, 64-deep
+ * K block) steps evenly, so a tile is cut into 1..n segments; segment j of a
+ * tile lands in ws slice j (ws holds n slices of N x M) and the segment
+ * counts in seg_table: [0] token-tile width, [1] token tiles, [2] weight rows
+ * per tile, [4 + m_tile * tiles + n_tile] segments. */
+int lpk_gemm_stream_k(const void* W, const void* X, float* ws, int M, int N, int K, int bn, int pair,
+                      const int* n_dev, int* seg_table, int max_ctas, void* stream);
+
 /* Time one projection of layer `layer` inside an instance (which: 0 QKV,
  * 1 O, 2 gate/up + SiLU, 3 down) at capacity t_cap with n_live live tokens:
  * *avg_ms = mean CUDA-event time over `iters` back-to-back launches. */

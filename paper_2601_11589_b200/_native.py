@@ -120,3 +120,4 @@ def _declare(L: ctypes.CDLL) -> None:
     sig("lpk_last_attention_schedule", c_i32, vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), ctypes.POINTER(c_i32))
     # kernel-level test hooks (include/laps_prefill_testing.h)
     sig("lpk_gemm", c_i32, vp, vp, vp, vp, vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, vp, vp, c_i32)
+    sig("lpk_gemm_stream_k", c_i32, vp, vp, vp, c_i32, c_i32, c_i32, c_i32, c_i32, vp, vp, c_i32, vp)

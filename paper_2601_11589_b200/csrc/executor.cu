@@ -94,6 +94,39 @@ static double partial_bytes_per_us() {
   return v;
 }
 
+// Stream-K (split-K-capable GEMMs, tensor-bound batches): groups of nt CTAs
+// (pairs) take equal shares `per` of the m_tiles x nk (weight tile, K-block)
+// steps, one token tile per member, so a one-wave GEMM (32B QKV / O at 512 tokens: 56 /
+// 40 tiles on 74 pairs) keeps every SM busy. Estimate: (per + 2 per segment)
+// steps at the tile width, plus the partial traffic: one extra fp32 tile per
+// share boundary, written by the GEMM and read back by the reduction kernel.
+static bool stream_k_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("LP_STREAMK");  // experiments: 0 = split-K plans only
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// Stream-K share of one worker group (one CTA (pair) per token tile, the
+// groups splitting the m_tiles x nk (weight tile, K-block) steps), and the
+// largest segment count of any tile; 0 groups: not runnable.
+long sk_share(int m_tiles, int n_tiles, int nk, int workers) {
+  const int groups = workers / n_tiles;
+  return groups < 1 ? 0 : (long(m_tiles) * nk + groups - 1) / groups;
+}
+int sk_max_segments(int m_tiles, int n_tiles, int nk, int workers) {
+  const long per = sk_share(m_tiles, n_tiles, nk, workers);
+  return per < 1 ? 1 << 20 : int((nk - 1) / per) + 2;
+}
+
+// CTA (pair) count of a launch: the grid gemm_launch sizes for the plan's
+// capacity (s_cap x m_tiles x nt_cap units, at most one per SM (pair)).
+int gemm_workers(int M, const GemmPlan& p, int sms) {
+  const long units = long(std::max(1, p.s_cap)) * (M / (128 * p.pair)) * p.nt_cap;
+  return int(std::min<long>(sms / p.pair, units));
+}
+
 TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms) {
   TilePlan t;
   const int base = std::max(1, (n_live + p.bn - 1) / p.bn);
@@ -104,6 +137,7 @@ TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms) {
   }
   const int workers = sms / p.pair, m_tiles = M / (128 * p.pair), nk = K / 64;
   const int nt_hi = std::min(p.nt_cap, (n_live + 15) / 16);
+  const int grid_workers = gemm_workers(M, p, sms);
   double best = 1e30;
   for (int nt = base; nt <= nt_hi; ++nt) {
     const int tw = ((n_live + nt - 1) / nt + 15) / 16 * 16;
@@ -117,6 +151,24 @@ TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms) {
         best = cost;
         t.n_tiles = nt;
         t.splits = s;
+        t.stream_k = false;
+      }
+    }
+    // Stream-K candidate: every tile's segments must fit the workspace slices.
+    // Measured to pay only between one and three 256-token tiles (deep-K
+    // down projections; profiles/r02_stream_k.txt), so it is offered there.
+    if (p.s_cap >= 2 && n_live > 256 && n_live <= 768 && stream_k_enabled() &&
+        sk_max_segments(m_tiles, nt, nk, grid_workers) <= p.s_cap) {
+      const long per = sk_share(m_tiles, nt, nk, grid_workers);
+      const double segs = double((per + nk - 1) / nk + 1);
+      const double extra = double(grid_workers - 1) * 128.0 * p.pair * tw * 8.0;  // partial bytes (bound)
+      const double cost = (double(per) + 2.0 * segs) * (tw + kTileOverheadCols) * kUsPerColKb +
+                          extra / partial_bytes_per_us();
+      if (cost < best * (1 - 1e-9)) {
+        best = cost;
+        t.n_tiles = nt;
+        t.splits = 1;
+        t.stream_k = true;
       }
     }
   }
@@ -286,6 +338,12 @@ void Instance::alloc_arena() {
     ws_elems_ = std::max(ws_elems_, mx * size_t(t));
   }
   ws_ = dmalloc<float>(ws_elems_, allocs_);
+  // Stream-K segment table (kSkTab*): one int per (128-row tile, 16-token tile) bounds it.
+  {
+    const size_t n = kSkTabHeader + size_t(std::max(qkv_out, h)) / 128 * size_t((t_max_ + 15) / 16);
+    sk_tab_ = dmalloc<int>(n, allocs_);
+    lp_check(cudaMemset(sk_tab_, 0, n * sizeof(int)), "memset sk table");
+  }
 
   // KV pool.
   page_elems_ = size_t(2) * m_.n_kv_heads * kPage * D;
@@ -417,6 +475,7 @@ void Instance::gemm(const CUtensorMap& tm_w, const GemmPlan& p, GemmArgs g, cons
   // With a device-side split count the grid is sized for the largest one allowed.
   g.splits = g.splits_dev ? p.s_cap : p.splits;
   g.n_tiles_cap = p.nt_cap;
+  if (g.splits_dev && g.mode == kEpiF32Partial) g.sk_tab = sk_tab_;  // metadata may select stream-K
   gemm_launch(tm_w, act_map(x, x_rows, g.K, gemm_b_box_rows(p.bn, p.pair)), g, p.bn, st, 0, p.pair);
 }
 
@@ -460,6 +519,7 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
       QkvCtx qc{n_tok, t_cap, nq, nkv, D, kPage, ws_, p.qkv.splits, md_.scalars + 4, size_t(t_cap), w.bqkv,
                 md_.positions, md_.slots, inv_freq_, q_, kv_layer};
       qc.s_cap = p.qkv.s_cap;
+      qc.sk_tab = sk_tab_;
       qkv_post(qc, st);
     }
     AttnCtx ac{md_.scalars + 2, md_.work, md_.scalars + 3, md_.combine, md_.q_start, md_.q_len, md_.hist,
@@ -483,7 +543,7 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
       g.splits_dev = md_.scalars + 5;
     }
     gemm(w.tm_o, p.o, g, attn_, t_max_, st);
-    resid_rmsnorm(rc, ws_, 0, o_fused ? nullptr : md_.scalars + 5, t_cap, x_resid_, w.g_mlp, x_norm_, st);
+    resid_rmsnorm(rc, ws_, 0, o_fused ? nullptr : md_.scalars + 5, sk_tab_, t_cap, x_resid_, w.g_mlp, x_norm_, st);
     // gate/up with fused SiLU*up.
     g = GemmArgs{};
     g.M = 2 * I; g.N = t_cap; g.K = h; g.n_dev = n_tok; g.ntiles_dev = md_.scalars + 10;
@@ -502,7 +562,7 @@ void Instance::enqueue_forward(int t_cap, int r_cap, cudaStream_t st, bool graph
     }
     gemm(w.tm_d, p.d, g, act_, t_max_, st);
     const bf16* g_next = (l + 1 < m_.layers) ? layers_[l + 1].g_attn : g_final_;
-    resid_rmsnorm(rc, ws_, 0, d_fused ? nullptr : md_.scalars + 6, t_cap, x_resid_, g_next, x_norm_, st);
+    resid_rmsnorm(rc, ws_, 0, d_fused ? nullptr : md_.scalars + 6, sk_tab_, t_cap, x_resid_, g_next, x_norm_, st);
     nvtxRangePop();
   }
   // Final norm already applied; LM head on the last real token per member —
@@ -831,9 +891,9 @@ int64_t Instance::submit(const lp_shape& shape, const lp_member* mem, int n, con
     const TilePlan to = live(sp.o, h, m_.n_q_heads * D, fuse_resid_ && sp.o.splits == 1);
     const TilePlan tg = live(sp.gu, 2 * m_.intermediate, h, true);
     const TilePlan td = live(sp.d, h, m_.intermediate, fuse_resid_ && sp.d.splits == 1);
-    mh_.scalars[4] = tq.splits;
-    mh_.scalars[5] = to.splits;
-    mh_.scalars[6] = td.splits;
+    mh_.scalars[4] = tq.meta_splits();
+    mh_.scalars[5] = to.meta_splits();
+    mh_.scalars[6] = td.meta_splits();
     mh_.scalars[8] = tq.n_tiles;
     mh_.scalars[9] = to.n_tiles;
     mh_.scalars[10] = tg.n_tiles;
@@ -946,14 +1006,19 @@ double Instance::time_gemm(int layer, int which, int t_cap, int n_live, int iter
   GemmPlan pl = *p;
   if (g.mode != kEpiF32Partial) pl.s_cap = 1;
   TilePlan tp = choose_tiles(g.M, g.K, pl, n_live, num_sms());
-  if (const char* e = std::getenv("LP_TIME_GEMM_PLAN")) {  // experiments: "n_tiles,splits"
+  if (const char* e = std::getenv("LP_TIME_GEMM_PLAN")) {  // experiments: "n_tiles,splits" (splits -1: stream-K)
     int nt = 0, s = 0;
-    if (std::sscanf(e, "%d,%d", &nt, &s) == 2 && nt >= 1 && nt <= pl.nt_cap && s >= 1 && s <= std::max(1, pl.s_cap)) {
+    const int gw = gemm_workers(g.M, pl, num_sms());
+    if (std::sscanf(e, "%d,%d", &nt, &s) == 2 && nt >= 1 && nt <= pl.nt_cap &&
+        ((s >= 1 && s <= std::max(1, pl.s_cap)) ||
+         (s == -1 && g.mode == kEpiF32Partial &&
+          sk_max_segments(g.M / (128 * pl.pair), nt, g.K / 64, gw) <= pl.s_cap))) {
       tp.n_tiles = nt;
-      tp.splits = s;
+      tp.splits = std::max(1, s);
+      tp.stream_k = s == -1;
     }
   }
-  mh_.scalars[4] = tp.splits;
+  mh_.scalars[4] = tp.meta_splits();
   mh_.scalars[8] = tp.n_tiles;
   g.ntiles_dev = md_.scalars + 8;
   if (g.mode == kEpiF32Partial) g.splits_dev = md_.scalars + 4;
@@ -1232,7 +1297,7 @@ int lpk_plan_gemm(int32_t M, int32_t K, int32_t t_cap, int32_t n_live, int32_t s
     if (bn) *bn = p.bn;
     if (pair) *pair = p.pair;
     if (n_tiles) *n_tiles = t.n_tiles;
-    if (splits) *splits = t.splits;
+    if (splits) *splits = t.meta_splits();  // -1: stream-K
   });
 }
 

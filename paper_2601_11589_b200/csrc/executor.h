@@ -68,6 +68,8 @@ struct GemmPlan {
 int choose_splits(int M, int bn, int pair, int n_live, int s_cap, int sms);
 struct TilePlan {
   int n_tiles = 1, splits = 1;
+  bool stream_k = false;  // stream-K over the flattened (tile, K-block) space (splits unused)
+  int meta_splits() const { return stream_k ? -1 : splits; }  // the device metadata value
 };
 TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms);
 GemmPlan plan_gemm_for_tests(int M, int K, int t_cap, bool allow_split, int sms);  // lpk_plan_gemm
@@ -178,6 +180,7 @@ class Instance {
   bf16 *x_norm_ = nullptr, *q_ = nullptr, *attn_ = nullptr, *act_ = nullptr, *x_last_ = nullptr;
   float* ws_ = nullptr;
   size_t ws_elems_ = 0;
+  int* sk_tab_ = nullptr;  // stream-K segment table (GemmArgs::sk_tab)
   float* logits_ = nullptr;
   unsigned long long* next_keys_ = nullptr;
   void* meta_dev_ = nullptr;

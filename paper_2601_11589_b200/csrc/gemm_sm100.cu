@@ -89,10 +89,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tw = min(BN, ((n_live + n_tiles - 1) / n_tiles + 15) / 16 * 16);
   const int num_kb = args.K / kBK;
   // Split-K factor: from device metadata when the plan is chosen per batch (pre-graph H2D).
-  const int splits = args.splits_dev ? max(1, *args.splits_dev) : args.splits;
+  const int split_raw = args.splits_dev ? *args.splits_dev : args.splits;
+  const bool sk = split_raw < 0 && args.sk_tab != nullptr;  // stream-K
+  const int splits = max(1, split_raw);
   const int units = splits * m_tiles * n_tiles;
   const int worker = blockIdx.x / kPair;        // CTA (pair) index
   const int n_workers = gridDim.x / kPair;
+  // Stream-K over the (weight tile, K-block) space, m-major: the workers form
+  // groups of one CTA (pair) per live token tile, group j owns steps
+  // [j*per, min((j+1)*per, total)) and its members run them in lockstep on
+  // their own token tiles, so every weight tile is fetched from DRAM once and
+  // shared through L2 (as consecutive split-K units are). Workers beyond the
+  // last whole group idle.
+  const int sk_tiles_n = (n_live + tw - 1) / tw;
+  const int sk_groups = max(1, n_workers / sk_tiles_n);
+  const int sk_total = m_tiles * num_kb;
+  const int sk_per = (sk_total + sk_groups - 1) / sk_groups;
+  const int sk_group = worker / sk_tiles_n, sk_n = worker % sk_tiles_n;
+  const int sk_beg = sk && sk_group < sk_groups ? min(sk_total, sk_group * sk_per) : 0;
+  const int sk_end = sk && sk_group < sk_groups ? min(sk_total, sk_beg + sk_per) : 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -119,16 +134,46 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // MMA N of the tile starting at n0 (a multiple of 16, <= tw).
   auto mma_n = [&](int n0) { return min(tw, (n_live - n0 + 15) / 16 * 16); };
-  auto decode = [&](int w, int& s, int& m0, int& n0, int& kb0, int& kb1) {
-    const int n = w % n_tiles;
-    const int rest = w / n_tiles;
-    const int m = rest % m_tiles;
-    s = rest / m_tiles;
-    m0 = m * kBM * kPair + static_cast<int>(rank) * kBM;  // this CTA's 128 weight rows
-    n0 = n * tw;
-    const int base = num_kb / splits, rem = num_kb % splits;
-    kb0 = s * base + min(s, rem);
-    kb1 = kb0 + base + (s < rem ? 1 : 0);
+  // One accumulation this CTA (pair) runs: output tile (m0, n0), K-blocks
+  // [kb0, kb1), written to ws slice s: split s (split-K) or, under stream-K,
+  // segment seg of the tile's nseg.
+  struct Seg { int s, m0, n0, kb0, kb1, seg, nseg, tile; };
+  // Iterators: `it` = next unit (split-K) or next flattened position (stream-K).
+  auto first_it = [&]() { return sk ? sk_beg : worker; };
+  auto next_seg = [&](int& it, Seg& g) -> bool {
+    if (sk) {
+      if (it >= sk_end) return false;
+      const int mt = it / num_kb;
+      g.kb0 = it % num_kb;
+      g.kb1 = min(num_kb, g.kb0 + (sk_end - it));
+      const int t0 = mt * num_kb;
+      g.seg = it / sk_per - t0 / sk_per;
+      g.nseg = (t0 + num_kb - 1) / sk_per - t0 / sk_per + 1;
+      it += g.kb1 - g.kb0;
+      g.s = g.seg;  // segment j of a tile -> ws slice j
+      g.tile = mt * sk_tiles_n + sk_n;
+      g.m0 = mt * kBM * kPair + static_cast<int>(rank) * kBM;
+      g.n0 = sk_n * tw;
+      return true;
+    }
+    while (it < units) {
+      const int w = it;
+      it += n_workers;
+      const int n = w % n_tiles;
+      const int rest = w / n_tiles;
+      const int m = rest % m_tiles;
+      g.s = rest / m_tiles;
+      g.m0 = m * kBM * kPair + static_cast<int>(rank) * kBM;  // this CTA's 128 weight rows
+      g.n0 = n * tw;
+      const int base = num_kb / splits, rem = num_kb % splits;
+      g.kb0 = g.s * base + min(g.s, rem);
+      g.kb1 = g.kb0 + base + (g.s < rem ? 1 : 0);
+      g.seg = 0;
+      g.nseg = 1;
+      g.tile = w;
+      if (g.n0 < n_live) return true;
+    }
+    return false;
   };
 
   if (warp == 0) {
@@ -160,32 +205,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       // Weight tiles do not depend on the previous kernel: fill the pipeline
       // with them before waiting on it (PDL), then add the activation tiles.
-      int pre = 0;
-      int pre_w = -1, pre_kb0 = 0, pre_n0 = 0;
-      for (int w = worker; w < units; w += n_workers) {
-        int s, m0, n0, kb0, kb1;
-        decode(w, s, m0, n0, kb0, kb1);
-        if (n0 >= n_live) continue;
-        pre_w = w; pre_kb0 = kb0; pre_n0 = n0;
-        pre = min(kb1 - kb0, C::kStages);
-        for (int i = 0; i < pre; ++i) {
-          expect(i);
-          load(i, kb0 + i, m0, n0, true, false);
-        }
-        break;
+      int it = first_it();
+      Seg g;
+      bool have = next_seg(it, g);
+      const int pre = have ? min(g.kb1 - g.kb0, C::kStages) : 0;
+      for (int i = 0; i < pre; ++i) {
+        expect(i);
+        load(i, g.kb0 + i, g.m0, g.n0, true, false);
       }
       pdl_wait();
-      for (int i = 0; i < pre; ++i) load(i, pre_kb0 + i, 0, pre_n0, false, true);
+      for (int i = 0; i < pre; ++i) load(i, g.kb0 + i, 0, g.n0, false, true);
       int stage = pre % C::kStages;
       uint32_t phase = pre == C::kStages ? 1u : 0u;
-      for (int w = (pre_w >= 0 ? pre_w : units); w < units; w += n_workers) {
-        int s, m0, n0, kb0, kb1;
-        decode(w, s, m0, n0, kb0, kb1);
-        if (n0 >= n_live) continue;
-        for (int kb = (w == pre_w ? kb0 + pre : kb0); kb < kb1; ++kb) {
+      for (int skip = pre; have; have = next_seg(it, g), skip = 0) {
+        for (int kb = g.kb0 + skip; kb < g.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           expect(stage);
-          load(stage, kb, m0, n0, true, true);
+          load(stage, kb, g.m0, g.n0, true, true);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -197,14 +233,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      for (int w = worker; w < units; w += n_workers) {
-        int s, m0, n0, kb0, kb1;
-        decode(w, s, m0, n0, kb0, kb1);
-        if (n0 >= n_live) continue;
+      int it = first_it();
+      Seg g;
+      while (next_seg(it, g)) {
+        const int kb0 = g.kb0, kb1 = g.kb1;
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        const uint32_t idesc = idesc_bf16(kBM * kPair, mma_n(n0));
+        const uint32_t idesc = idesc_bf16(kBM * kPair, mma_n(g.n0));
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -241,10 +277,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t aphase = 0;
     int sbuf = 0;
-    for (int w = worker; w < units; w += n_workers) {
-      int s, m0, n0, kb0, kb1;
-      decode(w, s, m0, n0, kb0, kb1);
-      if (n0 >= n_live) continue;
+    int it = first_it();
+    Seg g;
+    while (next_seg(it, g)) {
+      const int s = g.s, m0 = g.m0, n0 = g.n0;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int m = m0 + row;
@@ -253,6 +289,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (args.mode == kEpiBf16 && args.bias)
         bias = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(args.bias)[m]);
       const int ncols = min(tw, n_live - n0);  // live tokens of this tile
+      // Stream-K: record the tile's segment count once (its first segment),
+      // for the reduction kernel, which sums slices 0..nseg-1 in order.
+      if (sk && g.seg == 0 && et == 0) {
+        args.sk_tab[kSkTabHeader + g.tile] = g.nseg;
+        if (g.tile == 0) {
+          args.sk_tab[0] = tw;
+          args.sk_tab[1] = sk_tiles_n;
+          args.sk_tab[2] = kBM * kPair;
+        }
+      }
 #pragma unroll 1
       for (int c = 0; c < ncols; c += 16) {  // uniform across the epilogue group
         float v[16];
@@ -412,7 +458,9 @@ void launch_bn(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a
   using C = Cfg<BN, kPair>;
   auto* kern = gemm_bf16_tn_kernel<BN, kPair>;
   smem_attr_once(reinterpret_cast<const void*>(kern), C::kSmem);
-  const int units = a.splits * (a.M / (kBM * kPair)) * std::max((a.N + BN - 1) / BN, a.n_tiles_cap);
+  // Stream-K from the host (splits < 0): one CTA (pair) per SM (pair).
+  const int units = a.splits < 0 ? (1 << 30)
+                                 : a.splits * (a.M / (kBM * kPair)) * std::max((a.N + BN - 1) / BN, a.n_tiles_cap);
   int grid = num_sms() / kPair;
   if (max_ctas > 0 && max_ctas / kPair < grid) grid = max_ctas / kPair;
   if (units < grid) grid = units;
@@ -491,7 +539,10 @@ CUtensorMap make_tmap_3d_bf16(const void* ptr, const uint64_t dims[3], const uin
 
 void gemm_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, int bn,
                  cudaStream_t stream, int max_ctas, int pair) {
-  if (a.M % (kBM * pair) != 0 || a.K % kBK != 0 || a.N < 1 || a.splits < 1) {
+  const bool sk = a.splits < 0;
+  if (sk && (a.mode != kEpiF32Partial || !a.sk_tab || !a.ws))
+    throw std::runtime_error("gemm_launch: stream-K needs fp32 partial output, a workspace and a segment table");
+  if (a.M % (kBM * pair) != 0 || a.K % kBK != 0 || a.N < 1 || a.splits == 0) {
     throw std::runtime_error("gemm_launch: unsupported shape M=" + std::to_string(a.M) +
                              " K=" + std::to_string(a.K) + " N=" + std::to_string(a.N) +
                              " pair=" + std::to_string(pair));

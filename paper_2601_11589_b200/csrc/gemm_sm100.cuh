@@ -38,12 +38,24 @@ struct QkvEpi {
   int nq = 0, nkv = 0, page_size = 64;
 };
 
+// Stream-K segment table, written by the GEMM, read by the reduction kernels:
+// [0] token-tile width, [1] token tiles, [2] weight rows per tile, [3] unused,
+// [kSkTabHeader + m_tile * tiles + n_tile] segments of that output tile.
+constexpr int kSkTabHeader = 4;
+
 struct GemmArgs {
   int M = 0;            // weight rows (output features)
   int N = 0;            // token capacity (rows of X)
   int K = 0;            // reduction length (multiple of 64)
   int splits = 1;       // split-K factor
-  const int* splits_dev = nullptr;  // optional device-side split-K factor (overrides `splits`)
+  // Optional device-side split-K factor (overrides `splits`). A value < 0
+  // selects stream-K (kEpiF32Partial only): every CTA (pair) takes an equal
+  // share of the flattened (tile, K-block) space, so a tile is cut into 1..n
+  // segments at share boundaries; segment j lands in ws slice j and the
+  // tile's segment count in sk_tab, and the reduction kernel (qkv_post /
+  // resid_rmsnorm) sums slices 0..nseg-1 of each element in order.
+  const int* splits_dev = nullptr;
+  int* sk_tab = nullptr;  // stream-K segment table (layout: kSkTab*)
   const int* n_dev = nullptr;  // optional device-side live token count (<= N)
   // Optional device-side token-tile count (per-batch tile plan; clamped to
   // [ceil(n_live / bn), ceil(n_live / 16)]); n_tiles_cap bounds it for the grid.

@@ -2,6 +2,7 @@
 #include <cstdio>
 #include <stdexcept>
 
+#include "gemm_sm100.cuh"
 #include "launch.cuh"
 #include "ops.cuh"
 #include "synth.h"
@@ -78,29 +79,43 @@ __global__ void __launch_bounds__(kRowThreads)
 // All of a thread's loads (residual + every split) are issued before use.
 __global__ void __launch_bounds__(kRowThreads)
     resid_rmsnorm_kernel(RowCtx c, const float* __restrict__ ws, int splits, const int* splits_dev,
-                         size_t ws_stride_rows, float* __restrict__ x_resid, const bf16* __restrict__ gamma,
-                         bf16* __restrict__ x_norm) {
+                         const int* __restrict__ sk_tab, size_t ws_stride_rows, float* __restrict__ x_resid,
+                         const bf16* __restrict__ gamma, bf16* __restrict__ x_norm) {
   __shared__ float red[33];
   pdl_trigger();
   const int t = blockIdx.x;
   const bool live = t < *c.n_live;
-  if (splits_dev) splits = *splits_dev;  // pre-graph H2D metadata
+  if (splits_dev) splits = *splits_dev;  // pre-graph H2D metadata (< 0: stream-K)
   pdl_wait();
   if (!live) return;
   const int h4 = c.h / 4;
   float4* xr = reinterpret_cast<float4*>(x_resid + static_cast<size_t>(t) * c.h);
   float4 acc[kMaxVec];
+  int nseg[kMaxVec];  // slices to sum per float4 (stream-K: that output tile's segments)
+  int smax = max(1, splits);
 #pragma unroll
   for (int k = 0; k < kMaxVec; ++k) {
     const int i = threadIdx.x + k * kRowThreads;
     acc[k] = i < h4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    nseg[k] = max(1, splits);
   }
-  for (int s = 0; s < splits; ++s) {
+  if (splits < 0 && sk_tab) {  // written by the GEMM this kernel waited for
+    const int* seg = sk_tab + kSkTabHeader + t / sk_tab[0];
+    const int tiles = sk_tab[1], rows = sk_tab[2];
+    smax = 1;
+#pragma unroll
+    for (int k = 0; k < kMaxVec; ++k) {
+      const int i = threadIdx.x + k * kRowThreads;
+      nseg[k] = i < h4 ? seg[(4 * i / rows) * tiles] : 0;
+      smax = max(smax, nseg[k]);
+    }
+  }
+  for (int s = 0; s < smax; ++s) {
     const float4* p = reinterpret_cast<const float4*>(ws + (static_cast<size_t>(s) * ws_stride_rows + t) * c.h);
 #pragma unroll
     for (int k = 0; k < kMaxVec; ++k) {
       const int i = threadIdx.x + k * kRowThreads;
-      if (i < h4) {
+      if (i < h4 && s < nseg[k]) {
         const float4 q = p[i];
         acc[k].x += q.x; acc[k].y += q.y; acc[k].z += q.z; acc[k].w += q.w;
       }
@@ -186,7 +201,22 @@ __global__ void qkv_post_kernel(QkvCtx c) {
     s_sin[threadIdx.x] = sn;
   }
   pdl_wait();
-  const int splits = c.splits_dev ? max(1, *c.splits_dev) : c.splits;
+  const int raw = c.splits_dev ? *c.splits_dev : c.splits;
+  int nseg[U];  // slices to sum per unit (stream-K: that output tile's segments)
+  int splits = max(1, raw);
+#pragma unroll
+  for (int k = 0; k < U; ++k) nseg[k] = splits;
+  if (raw < 0 && c.sk_tab) {  // written by the GEMM this kernel waited for
+    const int* seg = c.sk_tab + kSkTabHeader + t / c.sk_tab[0];
+    const int tiles = c.sk_tab[1], rows = c.sk_tab[2];
+    splits = 1;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int u = threadIdx.x + k * blockDim.x;
+      nseg[k] = u < units ? seg[((u / upr) * c.d / rows) * tiles] : 0;
+      splits = max(splits, nseg[k]);
+    }
+  }
   for (int s0 = 0; s0 < splits; s0 += SU) {
     float4 p0[SU][U], p1[SU][U];
 #pragma unroll
@@ -195,7 +225,7 @@ __global__ void qkv_post_kernel(QkvCtx c) {
 #pragma unroll
       for (int k = 0; k < U; ++k) {
         const int u = threadIdx.x + k * blockDim.x;
-        if (u < units && s0 + e < splits) {
+        if (u < units && s0 + e < nseg[k]) {
           const int c0 = (u / upr) * c.d + (u % upr) * 4;
           p0[e][k] = *reinterpret_cast<const float4*>(row + c0);
           p1[e][k] = *reinterpret_cast<const float4*>(row + c0 + half);
@@ -206,7 +236,7 @@ __global__ void qkv_post_kernel(QkvCtx c) {
     for (int e = 0; e < SU; ++e) {
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        if (threadIdx.x + k * blockDim.x < units && s0 + e < splits) {
+        if (threadIdx.x + k * blockDim.x < units && s0 + e < nseg[k]) {
           add4(x0[k], p0[e][k]);
           add4(x1[k], p1[e][k]);
         }
@@ -362,10 +392,10 @@ __global__ void pdl_empty_kernel() {
 
 void launch_empty(dim3 grid, dim3 block, cudaStream_t st) { launch_k(pdl_empty_kernel, grid, block, 0, st); }
 
-void resid_rmsnorm(const RowCtx& c, const float* ws, int splits, const int* splits_dev, size_t ws_stride_rows,
-                   float* x_resid, const bf16* gamma, bf16* x_norm, cudaStream_t st) {
+void resid_rmsnorm(const RowCtx& c, const float* ws, int splits, const int* splits_dev, const int* sk_tab,
+                   size_t ws_stride_rows, float* x_resid, const bf16* gamma, bf16* x_norm, cudaStream_t st) {
   if (debug_empty("norm")) return launch_empty(dim3(c.t_cap), dim3(kRowThreads), st);
-  launch_k(resid_rmsnorm_kernel, dim3(c.t_cap), dim3(kRowThreads), 0, st, c, ws, splits, splits_dev,
+  launch_k(resid_rmsnorm_kernel, dim3(c.t_cap), dim3(kRowThreads), 0, st, c, ws, splits, splits_dev, sk_tab,
            ws_stride_rows, x_resid, gamma, x_norm);
 }
 

@@ -40,7 +40,8 @@ void embed_rmsnorm(const RowCtx& c, const int* tokens, const bf16* embed, const 
 
 // x_resid[t] += sum_s ws[s][t]; x_norm[t] = bf16(rmsnorm(x_resid[t]) * gamma)
 // splits_dev (optional): device-side split count overriding `splits`.
-void resid_rmsnorm(const RowCtx& c, const float* ws, int splits, const int* splits_dev, size_t ws_stride_rows,
+void resid_rmsnorm(const RowCtx& c, const float* ws, int splits, const int* splits_dev, const int* sk_tab,
+                   size_t ws_stride_rows,
                    float* x_resid, const bf16* gamma, bf16* x_norm, cudaStream_t st);
 
 struct QkvCtx {
@@ -59,6 +60,7 @@ struct QkvCtx {
   bf16* q_out;               // [T, nq*d]
   bf16* kv_layer;            // layer base of the paged cache
   int s_cap = 8;             // upper bound of the split count (picks the load schedule)
+  const int* sk_tab = nullptr;  // stream-K segment table (*splits_dev < 0; gemm_sm100.cuh kSkTab*)
 };
 // reduce splits + bias; RoPE(q, k); q -> q_out; k, v -> paged cache
 void qkv_post(const QkvCtx& c, cudaStream_t st);

@@ -118,3 +118,54 @@ def test_gemm_dynamic_tile_width(M, Ntok, K, bn, mode, splits, pair, n_live):
     _close(got, ref, n_live=n_live)
     if mode in (0, 3):
         assert torch.all(got[n_live:] == 0)
+
+
+@pytest.mark.parametrize("M,Ntok,K,bn,pair,n_live,max_ctas", [
+    (7168, 512, 5120, 256, 2, None, 0),    # 32B QKV at a 512-token chunk: 56 tiles on 74 pairs
+    (5120, 512, 5120, 256, 2, 500, 0),     # 32B O, live count below capacity
+    (5120, 512, 27648, 256, 2, None, 0),   # 32B down projection
+    (256, 64, 4096, 64, 1, None, 148),     # 2 tiles of 64 K blocks on 148 CTAs: 64 segments per tile
+    (1024, 600, 3584, 128, 2, 517, 20),    # 10 pairs, ragged live count
+])
+def test_gemm_stream_k(M, Ntok, K, bn, pair, n_live, max_ctas):
+    """Stream-K (csrc/gemm_sm100.cu): equal (weight tile, K-block) shares per
+    group of CTAs (pairs), one member per token tile; segment j of a tile lands in ws slice j and the segment counts in
+    the table the reduction kernels read. Summing each element's segments in
+    slice order reproduces the GEMM, every tile is covered, and the output is
+    bitwise reproducible run to run."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    W = (torch.randn(M, K, device="cuda", generator=g) * 0.05).bfloat16()
+    X = torch.randn(Ntok, K, device="cuda", generator=g).bfloat16()
+    live = n_live or Ntok
+    ref = X.float()[:live] @ W.float().t()
+    nd = torch.tensor([live], dtype=torch.int32, device="cuda")
+    workers = (max_ctas or torch.cuda.get_device_properties(0).multi_processor_count) // pair
+    nt = -(-live // bn)
+    tw = min(bn, (-(-live // nt) + 15) // 16 * 16)
+    tiles_n = -(-live // tw)
+    m_tiles = M // (128 * pair)
+    groups = workers // tiles_n  # one CTA (pair) per token tile, in lockstep
+    total = m_tiles * (K // 64)
+    per = -(-total // groups)
+    slices = (K // 64 - 1) // per + 2
+    ws = torch.full((slices, Ntok, M), float("nan"), device="cuda", dtype=torch.float32)
+    tab = torch.full((4 + (M // 128) * (-(-Ntok // 16)),), -1, dtype=torch.int32, device="cuda")
+    outs = []
+    for _ in range(3):
+        N.check(N.lib().lpk_gemm_stream_k(_ptr(W), _ptr(X), _ptr(ws), M, Ntok, K, bn, pair, _ptr(nd),
+                                          _ptr(tab), max_ctas, None))
+        torch.cuda.synchronize()
+        assert tab[:3].tolist() == [tw, tiles_n, 128 * pair]
+        nseg = tab[4:4 + m_tiles * tiles_n].view(m_tiles, tiles_n)
+        assert int(nseg.min()) >= 1 and int(nseg.max()) <= slices
+        # one extra segment per share boundary that falls inside a weight tile
+        assert int(nseg.sum()) - m_tiles * tiles_n == tiles_n * sum(1 for j in range(1, groups)
+                                                                    if j * per < total and (j * per) % (K // 64))
+        # element (t, f) sums the slices of its tile's segments, in order
+        per_elem = nseg.repeat_interleave(128 * pair, 0).repeat_interleave(tw, 1)[:M, :live].t()
+        out = ws[0, :live].clone()
+        for s_ in range(1, slices):
+            out = torch.where(per_elem > s_, out + ws[s_, :live], out)
+        outs.append(out)
+    _close(outs[0], ref)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])

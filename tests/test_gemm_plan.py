@@ -26,11 +26,22 @@ def plan(M, K, t_cap, n_live, sms=148, allow_split=True):
 
 def test_chunk_plans_512_tokens():
     # 512-token chunks: QKV and O run one K slice (5 slices made the reduction
-    # read 73 MB of partials), the down projection splits to fill the waves.
+    # read 73 MB of partials); the deep-K down projection runs stream-K
+    # (splits -1: equal K shares per CTA pair; 5 slices before, -10 %).
     assert plan(*SHAPES["qkv32"], 512, 512) == (256, 2, 2, 1)
     assert plan(*SHAPES["o32"], 512, 512)[2:] == (3, 1)
-    assert plan(*SHAPES["down32"], 512, 512)[2:] == (2, 5)
+    assert plan(*SHAPES["down32"], 512, 512)[2:] == (2, -1)
+    assert plan(*SHAPES["down7"], 384, 384)[3] == -1
     assert plan(*SHAPES["qkv7"], 512, 512)[3] == 1
+
+
+def test_stream_k_window():
+    # offered only between one and three 256-token tiles, never for fused
+    # epilogues (allow_split = 0) nor for weight-streaming batches
+    for name, (M, K) in SHAPES.items():
+        for t in (16, 128, 255, 256, 1024, 4096):
+            assert plan(M, K, t, t)[3] != -1
+        assert plan(M, K, 512, 512, allow_split=False)[3] == 1
 
 
 def test_split_bounds_and_fused_epilogues():
@@ -38,7 +49,7 @@ def test_split_bounds_and_fused_epilogues():
         for t in (16, 64, 256, 512, 1024, 4096):
             for n in sorted({1, t // 2, t}):
                 bn, pair, nt, s = plan(M, K, t, n)
-                assert 1 <= s <= 8 and s <= max(1, (K // 64) // 4) and s * t <= max(8192, t)
+                assert s == -1 or (1 <= s <= 8 and s <= max(1, (K // 64) // 4) and s * t <= max(8192, t))
                 assert pair in (1, 2) and bn in (16, 32, 64, 128, 256) and nt >= 1
                 assert plan(M, K, t, n, allow_split=False)[3] == 1
 
@@ -56,4 +67,4 @@ def test_partial_traffic_is_charged(t):
     # n_live), so the chosen split count never grows with n_live at a fixed
     # capacity.
     M, K = SHAPES["qkv32"]
-    assert plan(M, K, t, t)[3] <= plan(M, K, t, t // 2 + 128)[3]
+    assert 1 <= plan(M, K, t, t)[3] <= plan(M, K, t, t // 2 + 128)[3]
