@@ -25,11 +25,14 @@ namespace {
 
 constexpr int kBM = 128;            // weight rows per CTA (TMEM lanes)
 constexpr int kBK = 64;             // K per stage: one 128-byte swizzle row of bf16
-constexpr int kThreads = 192;       // warp0 TMA, warp1 MMA, warps2-5 epilogue
+constexpr int kThreads = 320;       // warp0 TMA, warp1 MMA, warps2-9 epilogue (two groups of 4)
+constexpr int kEpiWarps = 8;
 constexpr int kSmemBudget = 196 * 1024;
-// Epilogue staging, double-buffered: SiLU uses [16 tokens][64 features] bf16,
-// the fused QKV/RoPE epilogue [128 rows][17] fp32 (padded: conflict-free).
+// Epilogue staging, double-buffered per epilogue group: SiLU uses [16
+// tokens][64 features] bf16 (both groups), the fused QKV/RoPE epilogue [128
+// rows][17] fp32 (padded: conflict-free; group 0 only).
 constexpr int kEpiStageBytes = 128 * 17 * 4;
+constexpr int kEpiStage1Bytes = 16 * 64 * 2;
 
 template <int BN, int kPair>
 struct Cfg {
@@ -40,14 +43,40 @@ struct Cfg {
   static constexpr int kStages = (kSmemBudget / kStageBytes) > 8 ? 8 : (kSmemBudget / kStageBytes);
   static constexpr int kTmemCols = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int kBarBytes = 256;
-  static constexpr int kSmem = 1024 /*align*/ + kStages * kStageBytes + kBarBytes + 2 * kEpiStageBytes;
+  static constexpr int kSmem = 1024 /*align*/ + kStages * kStageBytes + kBarBytes + 2 * kEpiStageBytes +
+                               2 * kEpiStage1Bytes;
+  static_assert(kSmem <= 227 * 1024, "GEMM shared memory over the per-CTA limit");
 };
 
 // x * sigmoid(x) with the fast exp / divide intrinsics (|rel err| ~ 1e-7,
 // far below the bf16 rounding that follows).
 __device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// Named barrier of one epilogue group (ids 1, 2; 128 threads each).
+__device__ __forceinline__ void epi_bar(int group) { asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory"); }
+
+// Diagnostic build only (-DLP_GEMM_PROF, scripts/gemm_prof.py): %globaltimer
+// stamps of one launch's phases per CTA, recorded for the launch whose (M, K)
+// matches g_gemm_prof_sel. Compiled out of the product library.
+#ifdef LP_GEMM_PROF
+constexpr int kProfCtas = 160, kProfEv = 12;
+__device__ unsigned long long g_gemm_prof[kProfCtas][kProfEv];
+__device__ int g_gemm_prof_sel[2];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GEMM_PROF(ev)                                                                              \
+  do {                                                                                             \
+    if (args.M == g_gemm_prof_sel[0] && args.K == g_gemm_prof_sel[1] && blockIdx.x < kProfCtas) \
+      g_gemm_prof[blockIdx.x][ev] = gtimer();                                                      \
+  } while (0)
+#else
+#define GEMM_PROF(ev) \
+  do {                \
+  } while (0)
+#endif
 
 template <int BN, int kPair>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -70,6 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x % 32;
   const uint32_t rank = kPair == 2 ? cluster_rank() : 0;
   const bool leader = rank == 0;
+  if (threadIdx.x == 0) GEMM_PROF(0);  // entry
   pdl_trigger();
 
   // n_dev is written by the pre-graph H2D copy, never by a kernel: safe before pdl_wait.
@@ -118,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * kPair);  // every epilogue warp of the pair
+      mbar_init(&tempty[a], kEpiWarps * kPair);  // every epilogue warp of the pair
     }
     fence_mbar_init();
   }
@@ -131,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (kPair == 2) cluster_sync();  // peer barriers initialised before remote use
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) GEMM_PROF(1);  // barriers, TMEM, cluster ready
 
   // MMA N of the tile starting at n0 (a multiple of 16, <= tw).
   auto mma_n = [&](int n0) { return min(tw, (n_live - n0 + 15) / 16 * 16); };
@@ -214,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         load(i, g.kb0 + i, g.m0, g.n0, true, false);
       }
       pdl_wait();
+      GEMM_PROF(2);  // predecessor done
       for (int i = 0; i < pre; ++i) load(i, g.kb0 + i, 0, g.n0, false, true);
       int stage = pre % C::kStages;
       uint32_t phase = pre == C::kStages ? 1u : 0u;
@@ -225,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       }
+      GEMM_PROF(3);  // last load issued
     }
   } else if (warp == 1) {
     // ----------------------------------------------------------- MMA issuer (leader of a pair)
@@ -235,6 +268,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t aphase = 0;
       int it = first_it();
       Seg g;
+#ifdef LP_GEMM_PROF
+      int n_mma = 0;
+#endif
       while (next_seg(it, g)) {
         const int kb0 = g.kb0, kb1 = g.kb1;
         mbar_wait(&tempty[acc], aphase ^ 1);
@@ -244,6 +280,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+#ifdef LP_GEMM_PROF
+          if (n_mma++ == 0 && lane == 0) GEMM_PROF(4);  // first operands landed
+#endif
           if (elect_one()) {
             const uint64_t a_desc = sdesc_sw128(smem_u32(sA + stage * C::kABytes));
             const uint64_t b_desc = sdesc_sw128(smem_u32(sB + stage * C::kBBytes));
@@ -267,31 +306,54 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (++acc == 2) { acc = 0; aphase ^= 1; }
       }
+      if (lane == 0) GEMM_PROF(5);  // last MMA committed
     }
   } else {
     // ----------------------------------------------------------- epilogue
-    const int q = warp % 4;          // TMEM lane quarter this warp may touch
-    const int row = q * 32 + lane;   // tile row == TMEM lane
-    const int et = threadIdx.x - 64; // 0..127 within the epilogue group
+    // Two groups of 4 warps; each covers all 128 TMEM lanes (warp w may
+    // touch lanes 32*(w%4)..+31) and takes alternate 16-column chunks, so two
+    // warps per SM sub-partition hide each other's store latency. The fused
+    // QKV/RoPE epilogue (opt-in) runs on group 0 alone (its staging is 17 KB).
+    const int q = warp % 4;                 // TMEM lane quarter this warp may touch
+    const int row = q * 32 + lane;          // tile row == TMEM lane
+    const int eg = (warp - 2) / 4;          // epilogue group
+    const int et = threadIdx.x - 64 - eg * 128;  // 0..127 within the group
+    const bool solo = args.mode == kEpiQkvRope;
+    const int c_first = solo ? 0 : eg * 16, c_step = solo ? 16 : 32;
+    const bool idle = solo && eg == 1;
+    __nv_bfloat16* const stage_g =
+        eg == 0 ? epi_stage : reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(epi_stage) + 2 * kEpiStageBytes);
     const uint32_t tempty_leader = kPair == 2 ? mapa(smem_u32(&tempty[0]), 0) : 0;
     int acc = 0;
     uint32_t aphase = 0;
     int sbuf = 0;
     int it = first_it();
     Seg g;
+#ifdef LP_GEMM_PROF
+    int n_epi = 0;
+#endif
     while (next_seg(it, g)) {
       const int s = g.s, m0 = g.m0, n0 = g.n0;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
+#ifdef LP_GEMM_PROF
+      if (et == 0 && eg == 0) {
+        if (n_epi == 0) GEMM_PROF(6);  // first accumulator ready
+        GEMM_PROF(8);                  // last accumulator ready (overwritten per unit)
+      }
+      ++n_epi;
+#endif
       const int m = m0 + row;
       const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       float bias = 0.f;
       if (args.mode == kEpiBf16 && args.bias)
         bias = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(args.bias)[m]);
       const int ncols = min(tw, n_live - n0);  // live tokens of this tile
+      const size_t ldm = static_cast<size_t>(args.M);
+      float* const ws_unit = args.ws + static_cast<size_t>(s) * args.ws_stride * ldm + m;  // fp32 partial modes
       // Stream-K: record the tile's segment count once (its first segment),
       // for the reduction kernel, which sums slices 0..nseg-1 in order.
-      if (sk && g.seg == 0 && et == 0) {
+      if (sk && g.seg == 0 && et == 0 && eg == 0) {
         args.sk_tab[kSkTabHeader + g.tile] = g.nseg;
         if (g.tile == 0) {
           args.sk_tab[0] = tw;
@@ -299,18 +361,40 @@ __global__ void __launch_bounds__(kThreads, 1)
           args.sk_tab[2] = kBM * kPair;
         }
       }
+#ifdef LP_GEMM_PROF
+      long long p_ld = 0, p_st = 0, p_t = clock64();
+#endif
+      // TMEM loads run one 16-column chunk ahead of the stores: the next
+      // chunk's round trip overlaps this chunk's global writes.
+      const int c_end = idle ? 0 : ncols;
+      uint32_t nxt[16];
+      if (c_first < c_end) tmem_ld16_issue(t_addr + c_first, nxt);
 #pragma unroll 1
-      for (int c = 0; c < ncols; c += 16) {  // uniform across the epilogue group
+      for (int c = c_first; c < c_end; c += c_step) {  // uniform across the epilogue group
         float v[16];
-        tmem_ld16(t_addr + c, v);
+        tmem_ld16_wait(nxt);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(nxt[j]);
+        if (c + c_step < c_end) tmem_ld16_issue(t_addr + c + c_step, nxt);
+#ifdef LP_GEMM_PROF
+        { const long long now = clock64(); p_ld += now - p_t; p_t = now; }
+#endif
         const int nbase = n0 + c;
         const int cnt = min(16, ncols - c);
         if (args.mode == kEpiF32Partial) {
-          // 32 lanes x consecutive m: one full 128-byte line per token.
-          float* dst = args.ws + (static_cast<size_t>(s) * args.ws_stride + nbase) * args.M + m;
+          // 32 lanes x consecutive m: one full 128-byte line per token. One
+          // warp per SM sub-partition runs this, so it is latency-bound:
+          // every address is an independent offset from one base (no
+          // dependent chains), and full chunks store unpredicated.
+          float* dst = ws_unit + static_cast<size_t>(nbase) * ldm;
+          if (cnt == 16) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (j < cnt) dst[static_cast<size_t>(j) * args.M] = v[j];
+            for (int j = 0; j < 16; ++j) dst[j * ldm] = v[j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < cnt) dst[j * ldm] = v[j];
+          }
         } else if (args.mode == kEpiSiluMul) {
           // Even row = gate, odd row = up of feature m/2. Stage the 64-feature x
           // 16-token block in smem, then write 128-byte token rows with 16-byte
@@ -318,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // Lane pair (2f, 2f+1) holds gate / up of feature f for 16 tokens.
           // One shuffle per two tokens: the even lane finishes token j, the
           // odd lane token j+1, so every lane does useful work.
-          __nv_bfloat16* stg = epi_stage + sbuf * (16 * 64);
+          __nv_bfloat16* stg = stage_g + sbuf * (16 * 64);
           const bool odd = lane & 1;
 #pragma unroll
           for (int j = 0; j < 16; j += 2) {
@@ -328,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float u = __bfloat162float(__float2bfloat16_rn(odd ? v[j + 1] : other));
             stg[(j + (odd ? 1 : 0)) * 64 + (row >> 1)] = __float2bfloat16_rn(silu(g) * u);
           }
-          epi_bar();
+          epi_bar(eg);
           const int tj = et >> 3, seg = et & 7;
           if (tj < cnt) {
             const uint4 val = *reinterpret_cast<const uint4*>(stg + tj * 64 + seg * 8);
@@ -364,10 +448,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] += b;
           if (hd < e.nq + e.nkv) {  // uniform per CTA
-            float* xs = reinterpret_cast<float*>(epi_stage) + sbuf * (128 * 17);
+            float* xs = reinterpret_cast<float*>(stage_g) + sbuf * (128 * 17);
 #pragma unroll
             for (int j = 0; j < 16; ++j) xs[row * 17 + j] = v[j];
-            epi_bar();
+            epi_bar(eg);
             const int prow = row ^ 64;
             const float f = e.inv_freq[row & 63];
             const float sgn = row < 64 ? -1.f : 1.f;
@@ -411,7 +495,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 16; ++j)
             if (j < cnt) dst[static_cast<size_t>(j) * args.ldo] = v[j];
         }
+#ifdef LP_GEMM_PROF
+        { const long long now = clock64(); p_st += now - p_t; p_t = now; }
+#endif
       }
+#ifdef LP_GEMM_PROF
+      if (et == 0 && eg == 0 && args.M == g_gemm_prof_sel[0] && args.K == g_gemm_prof_sel[1] && blockIdx.x < kProfCtas) {
+        g_gemm_prof[blockIdx.x][10] = p_ld;
+        g_gemm_prof[blockIdx.x][11] = p_st;
+      }
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -420,6 +513,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
+#ifdef LP_GEMM_PROF
+    if (et == 0 && eg == 0) {
+      GEMM_PROF(7);  // epilogue done
+      if (args.M == g_gemm_prof_sel[0] && args.K == g_gemm_prof_sel[1] && blockIdx.x < kProfCtas)
+        g_gemm_prof[blockIdx.x][9] = n_epi;
+    }
+#endif
   }
 
   tc_fence_before();
@@ -487,6 +587,17 @@ void launch_bn(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a
 }
 
 }  // namespace
+
+#ifdef LP_GEMM_PROF
+extern "C" int lp_debug_gemm_prof(unsigned long long* out, size_t n, int M, int K) {
+  const int sel[2] = {M, K};
+  static unsigned long long zero[kProfCtas][kProfEv];
+  const size_t bytes = std::min(n * sizeof(unsigned long long), sizeof(g_gemm_prof));
+  if (out && cudaMemcpyFromSymbol(out, g_gemm_prof, bytes) != cudaSuccess) return -1;
+  if (cudaMemcpyToSymbol(g_gemm_prof, zero, sizeof(zero)) != cudaSuccess) return -1;
+  return cudaMemcpyToSymbol(g_gemm_prof_sel, sel, sizeof(sel)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 int num_sms() {
   // Per device: a process may drive several GPUs (one instance each).
