@@ -91,6 +91,7 @@ __device__ __forceinline__ uint32_t tile_addr(uint32_t base, int r, int c) {
 // bf16 rounding of P flips no more often than with ex2.approx; the cubic
 // used before (2.1e-4) flipped ~2% of the P values it produced).
 // Inputs are clamped at -126 (-inf -> 2^-126).
+
 __device__ __forceinline__ float ex2_poly(float x) {
   x = fmaxf(x, -126.f);
   const float t = x + 12582912.f;
@@ -101,6 +102,93 @@ __device__ __forceinline__ float ex2_poly(float x) {
   p = fmaf(p, f, 0.69314694f);
   p = fmaf(p, f, 1.0000001f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// Packed fp32x2 arithmetic (FFMA2 / FADD2: two lanes per FMA-pipe issue).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n"
+      " mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n mov.b64 rc, {%6, %7};\n"
+      " fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n"
+      " mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// ex2_poly on a pair, packed (same operations per lane, so bit-identical).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  constexpr float kMagic = 12582912.f;
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = fadd2(x, make_float2(kMagic, kMagic));
+  const float2 u = fadd2(t, make_float2(-kMagic, -kMagic));
+  const float2 f = ffma2(u, make_float2(-1.f, -1.f), x);
+  float2 p = ffma2(make_float2(0.0013276408f, 0.0013276408f), f, make_float2(0.0096755205f, 0.0096755205f));
+  p = ffma2(p, f, make_float2(0.055507131f, 0.055507131f));
+  p = ffma2(p, f, make_float2(0.24022120f, 0.24022120f));
+  p = ffma2(p, f, make_float2(0.69314694f, 0.69314694f));
+  p = ffma2(p, f, make_float2(1.0000001f, 1.0000001f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+// Row max of a thread's slice: three-input max, two independent chains.
+template <int N>
+__device__ __forceinline__ float slice_max(const float (&v)[N]) {
+  float a = -INFINITY, b = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < N; k += 4) {
+    a = fmax3(a, v[k], v[k + 1]);
+    b = fmax3(b, v[k + 2], v[k + 3]);
+  }
+  return fmaxf(a, b);
+}
+
+// Softmax numerators of a thread's slice in place, 2^(s * scale - m), and
+// their sum. The scale, the sum and the FMA-pipe exponentials run packed
+// (fp32x2); pair q = (2q, 2q+1) goes to the polynomial iff q % kExpPairMod <
+// kExpPairCnt, the rest to MUFU ex2 (the step is bound by FMA-pipe issue
+// and MUFU throughput together; profiles/r02_attn_experiments.md).
+#ifndef LP_EXP_PAIR_MOD
+#define LP_EXP_PAIR_MOD 8
+#define LP_EXP_PAIR_CNT 3
+#endif
+constexpr int kExpPairMod = LP_EXP_PAIR_MOD, kExpPairCnt = LP_EXP_PAIR_CNT;
+template <int N>
+__device__ __forceinline__ float slice_exp_sum(float (&v)[N], float scale, float m_use) {
+  const float2 sc2 = make_float2(scale, scale), mm2 = make_float2(-m_use, -m_use);
+  float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int q = 0; q < N / 2; ++q) {
+    const float2 x = ffma2(make_float2(v[2 * q], v[2 * q + 1]), sc2, mm2);
+    float2 e;
+    if (q % kExpPairMod < kExpPairCnt) {
+      e = ex2_poly2(x);
+    } else {
+      e.x = ex2_ftz(x.x);
+      e.y = ex2_ftz(x.y);
+    }
+    v[2 * q] = e.x;
+    v[2 * q + 1] = e.y;
+    if (q & 1) s1 = fadd2(s1, e);
+    else s0 = fadd2(s0, e);
+  }
+  const float2 s = fadd2(s0, s1);
+  return s.x + s.y;
 }
 
 // Diagnostic build only (-DLP_ATTN_PROF, scripts/attn_prof.py): clock64
@@ -313,17 +401,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       const int kbase = (t_begin + 2 * s) * 64 + grp * kHalf;
       const int kvalid = min(kKeys, (t_end - t_begin - 2 * s) * 64) - grp * kHalf;  // keys of real pages
-      float mx = -INFINITY;
-      if (kvalid >= kHalf && kbase + kHalf - 1 <= pos) {  // whole half visible: no mask (the bulk of long histories)
+      if (!(kvalid >= kHalf && kbase + kHalf - 1 <= pos)) {  // a whole visible half needs no mask (long histories)
 #pragma unroll
-        for (int k = 0; k < kHalf; ++k) mx = fmaxf(mx, sc[k]);
-      } else {
-#pragma unroll
-        for (int k = 0; k < kHalf; ++k) {
+        for (int k = 0; k < kHalf; ++k)
           if (k >= kvalid || kbase + k > pos) sc[k] = -INFINITY;
-          mx = fmaxf(mx, sc[k]);
-        }
       }
+      float mx = slice_max(sc);
       const uint32_t rb = red + (s & 1) * 2 * kRows * 4;
       st_shared_f32(rb + (grp * kRows + rt) * 4, mx);
       pair_sync();
@@ -335,19 +418,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float m_use = m_new == -INFINITY ? 0.f : m_new;
       const float corr = grow ? exp2f(m_run - m_use) : 1.f;
       m_run = m_new;
-      float sum = 0.f;
-      // ex2.approx.ftz: one MUFU op per element. exp2f adds a range check and
-      // two conditional scalings per element (denormal results), ~3 extra
-      // issue slots each; arguments here are <= kRescaleTau and results below
-      // 2^-126 are negligible against the row sum.
-      // One in three on the FMA pipe (ex2_poly): a step's 16384 exponentials
-      // are otherwise MUFU-throughput-bound (16/clk/SM).
-#pragma unroll
-      for (int k = 0; k < kHalf; ++k) {
-        const float x = sc[k] * c.scale_log2 - m_use;
-        sc[k] = (k % 3 == 2) ? ex2_poly(x) : ex2_ftz(x);
-        sum += sc[k];
-      }
+      // ex2.approx.ftz (MUFU) for most elements: exp2f adds a range check and
+      // two conditional scalings per element; arguments here are <=
+      // kRescaleTau and results below 2^-126 are negligible against the row
+      // sum. 3 pairs in 8 run the polynomial on the FMA pipe (slice_exp_sum).
+      const float sum = slice_exp_sum(sc, c.scale_log2, m_use);
       l_run = l_run * corr + sum;
       if (prof_me) ATTN_PROF(1, s, 2);
 
@@ -666,17 +741,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         const int kbase = (pc.t_begin + 2 * s) * 64 + grp * kHalf;
         const int kvalid = min(kKeys, (pc.t_end - pc.t_begin - 2 * s) * 64) - grp * kHalf;
-        float mx = -INFINITY;
-        if (kvalid >= kHalf && kbase + kHalf - 1 <= pos) {
+        if (!(kvalid >= kHalf && kbase + kHalf - 1 <= pos)) {
 #pragma unroll
-          for (int k = 0; k < kHalf; ++k) mx = fmaxf(mx, sc[k]);
-        } else {
-#pragma unroll
-          for (int k = 0; k < kHalf; ++k) {
+          for (int k = 0; k < kHalf; ++k)
             if (k >= kvalid || kbase + k > pos) sc[k] = -INFINITY;
-            mx = fmaxf(mx, sc[k]);
-          }
         }
+        float mx = slice_max(sc);
         const uint32_t rb = red + (x & 1) * 2 * kRows * 4;
         st_shared_f32(rb + (grp * kRows + rt) * 4, mx);
         pair_sync();
@@ -687,13 +757,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float m_use = m_new == -INFINITY ? 0.f : m_new;
         const float corr = grow ? exp2f(m_run - m_use) : 1.f;
         m_run = m_new;
-        float sum = 0.f;
-#pragma unroll
-        for (int k = 0; k < kHalf; ++k) {
-          const float xv = sc[k] * c.scale_log2 - m_use;
-          sc[k] = (k % 3 == 2) ? ex2_poly(xv) : ex2_ftz(xv);
-          sum += sc[k];
-        }
+        const float sum = slice_exp_sum(sc, c.scale_log2, m_use);
         l_run = l_run * corr + sum;
         if (x >= 2) {  // P buffer st was read by PV(x - 2)
           mbar_wait(&p_free[st], ((x >> 1) & 1) ^ 1);

@@ -100,10 +100,10 @@ static double partial_bytes_per_us() {
 // 40 tiles on 74 pairs) keeps every SM busy. Estimate: (per + 2 per segment)
 // steps at the tile width, plus the partial traffic: one extra fp32 tile per
 // share boundary, written by the GEMM and read back by the reduction kernel.
-static bool stream_k_enabled() {
-  static const bool v = [] {
-    const char* e = std::getenv("LP_STREAMK");  // experiments: 0 = split-K plans only
-    return !(e && e[0] == '0');
+static int stream_k_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("LP_STREAMK");  // experiments: 0 = split-K plans only, 2 = stream-K wherever it fits
+    return e ? std::atoi(e) : 1;
   }();
   return v;
 }
@@ -157,14 +157,16 @@ TilePlan choose_tiles(int M, int K, const GemmPlan& p, int n_live, int sms) {
     // Stream-K candidate: every tile's segments must fit the workspace slices.
     // Measured to pay only between one and three 256-token tiles (deep-K
     // down projections; profiles/r02_stream_k.txt), so it is offered there.
-    if (p.s_cap >= 2 && n_live > 256 && n_live <= 768 && stream_k_enabled() &&
+    const int skm = stream_k_mode();
+    if (p.s_cap >= 2 && ((n_live > 256 && n_live <= 768 && skm == 1) || skm == 2) &&
         sk_max_segments(m_tiles, nt, nk, grid_workers) <= p.s_cap) {
       const long per = sk_share(m_tiles, nt, nk, grid_workers);
       const double segs = double((per + nk - 1) / nk + 1);
       const double extra = double(grid_workers - 1) * 128.0 * p.pair * tw * 8.0;  // partial bytes (bound)
-      const double cost = (double(per) + 2.0 * segs) * (tw + kTileOverheadCols) * kUsPerColKb +
-                          extra / partial_bytes_per_us();
-      if (cost < best * (1 - 1e-9)) {
+      const double cost = skm == 2 ? -1.0
+                                   : (double(per) + 2.0 * segs) * (tw + kTileOverheadCols) * kUsPerColKb +
+                                         extra / partial_bytes_per_us();
+      if (skm == 2 ? !t.stream_k : cost < best * (1 - 1e-9)) {
         best = cost;
         t.n_tiles = nt;
         t.splits = 1;

@@ -25,8 +25,16 @@ namespace {
 
 constexpr int kBM = 128;            // weight rows per CTA (TMEM lanes)
 constexpr int kBK = 64;             // K per stage: one 128-byte swizzle row of bf16
-constexpr int kThreads = 320;       // warp0 TMA, warp1 MMA, warps2-9 epilogue (two groups of 4)
-constexpr int kEpiWarps = 8;
+// Epilogue warp groups of 4 (each covers all 128 TMEM lanes, alternate
+// 16-column chunks). Two groups halve the last tile's epilogue in isolation
+// but cost ~1.5 % on whole bucket forwards (8 more warps polling barriers
+// next to the TMA / MMA warps; profiles/r02_gemm_timeline.md), so one is built.
+#ifndef LP_GEMM_EPI_GROUPS
+#define LP_GEMM_EPI_GROUPS 1
+#endif
+constexpr int kEpiGroups = LP_GEMM_EPI_GROUPS;
+constexpr int kThreads = 64 + 128 * kEpiGroups;  // warp0 TMA, warp1 MMA, then the epilogue groups
+constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kSmemBudget = 196 * 1024;
 // Epilogue staging, double-buffered per epilogue group: SiLU uses [16
 // tokens][64 features] bf16 (both groups), the fused QKV/RoPE epilogue [128
@@ -44,7 +52,7 @@ struct Cfg {
   static constexpr int kTmemCols = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int kBarBytes = 256;
   static constexpr int kSmem = 1024 /*align*/ + kStages * kStageBytes + kBarBytes + 2 * kEpiStageBytes +
-                               2 * kEpiStage1Bytes;
+                               (kEpiGroups - 1) * 2 * kEpiStage1Bytes;
   static_assert(kSmem <= 227 * 1024, "GEMM shared memory over the per-CTA limit");
 };
 
@@ -310,16 +318,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ----------------------------------------------------------- epilogue
-    // Two groups of 4 warps; each covers all 128 TMEM lanes (warp w may
-    // touch lanes 32*(w%4)..+31) and takes alternate 16-column chunks, so two
-    // warps per SM sub-partition hide each other's store latency. The fused
-    // QKV/RoPE epilogue (opt-in) runs on group 0 alone (its staging is 17 KB).
+    // Groups of 4 warps; each covers all 128 TMEM lanes (warp w may touch
+    // lanes 32*(w%4)..+31) and takes every kEpiGroups-th 16-column chunk. The
+    // fused QKV/RoPE epilogue (opt-in) runs on group 0 alone (its staging is 17 KB).
     const int q = warp % 4;                 // TMEM lane quarter this warp may touch
     const int row = q * 32 + lane;          // tile row == TMEM lane
     const int eg = (warp - 2) / 4;          // epilogue group
     const int et = threadIdx.x - 64 - eg * 128;  // 0..127 within the group
     const bool solo = args.mode == kEpiQkvRope;
-    const int c_first = solo ? 0 : eg * 16, c_step = solo ? 16 : 32;
+    const int c_first = solo ? 0 : eg * 16, c_step = solo ? 16 : 16 * kEpiGroups;
     const bool idle = solo && eg == 1;
     __nv_bfloat16* const stage_g =
         eg == 0 ? epi_stage : reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(epi_stage) + 2 * kEpiStageBytes);

@@ -91,33 +91,43 @@ __global__ void __launch_bounds__(kRowThreads)
   const int h4 = c.h / 4;
   float4* xr = reinterpret_cast<float4*>(x_resid + static_cast<size_t>(t) * c.h);
   float4 acc[kMaxVec];
-  int nseg[kMaxVec];  // slices to sum per float4 (stream-K: that output tile's segments)
-  int smax = max(1, splits);
 #pragma unroll
   for (int k = 0; k < kMaxVec; ++k) {
     const int i = threadIdx.x + k * kRowThreads;
     acc[k] = i < h4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    nseg[k] = max(1, splits);
   }
-  if (splits < 0 && sk_tab) {  // written by the GEMM this kernel waited for
+  if (splits >= 0 || !sk_tab) {  // split-K: every element sums `splits` slices
+    for (int s = 0; s < splits; ++s) {
+      const float4* p = reinterpret_cast<const float4*>(ws + (static_cast<size_t>(s) * ws_stride_rows + t) * c.h);
+#pragma unroll
+      for (int k = 0; k < kMaxVec; ++k) {
+        const int i = threadIdx.x + k * kRowThreads;
+        if (i < h4) {
+          const float4 q = p[i];
+          acc[k].x += q.x; acc[k].y += q.y; acc[k].z += q.z; acc[k].w += q.w;
+        }
+      }
+    }
+  } else {  // stream-K: the segments of each element's output tile (table written by the GEMM)
     const int* seg = sk_tab + kSkTabHeader + t / sk_tab[0];
     const int tiles = sk_tab[1], rows = sk_tab[2];
-    smax = 1;
+    int nseg[kMaxVec];
+    int smax = 1;
 #pragma unroll
     for (int k = 0; k < kMaxVec; ++k) {
       const int i = threadIdx.x + k * kRowThreads;
       nseg[k] = i < h4 ? seg[(4 * i / rows) * tiles] : 0;
       smax = max(smax, nseg[k]);
     }
-  }
-  for (int s = 0; s < smax; ++s) {
-    const float4* p = reinterpret_cast<const float4*>(ws + (static_cast<size_t>(s) * ws_stride_rows + t) * c.h);
+    for (int s = 0; s < smax; ++s) {
+      const float4* p = reinterpret_cast<const float4*>(ws + (static_cast<size_t>(s) * ws_stride_rows + t) * c.h);
 #pragma unroll
-    for (int k = 0; k < kMaxVec; ++k) {
-      const int i = threadIdx.x + k * kRowThreads;
-      if (i < h4 && s < nseg[k]) {
-        const float4 q = p[i];
-        acc[k].x += q.x; acc[k].y += q.y; acc[k].z += q.z; acc[k].w += q.w;
+      for (int k = 0; k < kMaxVec; ++k) {
+        const int i = threadIdx.x + k * kRowThreads;
+        if (i < h4 && s < nseg[k]) {
+          const float4 q = p[i];
+          acc[k].x += q.x; acc[k].y += q.y; acc[k].z += q.z; acc[k].w += q.w;
+        }
       }
     }
   }
@@ -202,46 +212,50 @@ __global__ void qkv_post_kernel(QkvCtx c) {
   }
   pdl_wait();
   const int raw = c.splits_dev ? *c.splits_dev : c.splits;
-  int nseg[U];  // slices to sum per unit (stream-K: that output tile's segments)
-  int splits = max(1, raw);
+  // Sum `bound` slices; unit k takes the first nseg_of(k) of them.
+  auto reduce = [&](int bound, auto nseg_of) {
+    for (int s0 = 0; s0 < bound; s0 += SU) {
+      float4 p0[SU][U], p1[SU][U];
 #pragma unroll
-  for (int k = 0; k < U; ++k) nseg[k] = splits;
-  if (raw < 0 && c.sk_tab) {  // written by the GEMM this kernel waited for
+      for (int e = 0; e < SU; ++e) {
+        const float* row = c.ws + (static_cast<size_t>(s0 + e) * c.ws_stride_rows + t) * qkv_out;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int u = threadIdx.x + k * blockDim.x;
+          if (u < units && s0 + e < nseg_of(k)) {
+            const int c0 = (u / upr) * c.d + (u % upr) * 4;
+            p0[e][k] = *reinterpret_cast<const float4*>(row + c0);
+            p1[e][k] = *reinterpret_cast<const float4*>(row + c0 + half);
+          }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < SU; ++e) {
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          if (threadIdx.x + k * blockDim.x < units && s0 + e < nseg_of(k)) {
+            add4(x0[k], p0[e][k]);
+            add4(x1[k], p1[e][k]);
+          }
+        }
+      }
+    }
+  };
+  if (raw >= 0 || !c.sk_tab) {  // split-K: every unit sums the same slices
+    const int splits = max(1, raw);
+    reduce(splits, [&](int) { return splits; });
+  } else {  // stream-K: the segments of each unit's output tile (table written by the GEMM)
     const int* seg = c.sk_tab + kSkTabHeader + t / c.sk_tab[0];
     const int tiles = c.sk_tab[1], rows = c.sk_tab[2];
-    splits = 1;
+    int nseg[U];
+    int bound = 1;
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const int u = threadIdx.x + k * blockDim.x;
       nseg[k] = u < units ? seg[((u / upr) * c.d / rows) * tiles] : 0;
-      splits = max(splits, nseg[k]);
+      bound = max(bound, nseg[k]);
     }
-  }
-  for (int s0 = 0; s0 < splits; s0 += SU) {
-    float4 p0[SU][U], p1[SU][U];
-#pragma unroll
-    for (int e = 0; e < SU; ++e) {
-      const float* row = c.ws + (static_cast<size_t>(s0 + e) * c.ws_stride_rows + t) * qkv_out;
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int u = threadIdx.x + k * blockDim.x;
-        if (u < units && s0 + e < nseg[k]) {
-          const int c0 = (u / upr) * c.d + (u % upr) * 4;
-          p0[e][k] = *reinterpret_cast<const float4*>(row + c0);
-          p1[e][k] = *reinterpret_cast<const float4*>(row + c0 + half);
-        }
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < SU; ++e) {
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        if (threadIdx.x + k * blockDim.x < units && s0 + e < nseg[k]) {
-          add4(x0[k], p0[e][k]);
-          add4(x1[k], p1[e][k]);
-        }
-      }
-    }
+    reduce(bound, [&](int k) { return nseg[k]; });
   }
   __syncthreads();
   const int slot = c.slot_mapping[t];
