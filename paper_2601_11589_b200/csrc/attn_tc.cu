@@ -732,9 +732,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&s_full[st], (x >> 1) & 1);
         tc_fence_after();
         float sc[kHalf];
+        {  // all four S loads in flight before the first wait
+          uint32_t r[kHalf / 16][16];
 #pragma unroll
-        for (int cc = 0; cc < kHalf / 16; ++cc)
-          tmem_ld16(tmem + lane_off + st * kKeys + grp * kHalf + cc * 16, sc + cc * 16);
+          for (int cc = 0; cc < kHalf / 16; ++cc) tmem_ld16_issue(tmem + lane_off + st * kKeys + grp * kHalf + cc * 16, r[cc]);
+#pragma unroll
+          for (int cc = 0; cc < kHalf / 16; ++cc) {
+            tmem_ld16_wait(r[cc]);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) sc[cc * 16 + q] = __uint_as_float(r[cc][q]);
+          }
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[st]);
