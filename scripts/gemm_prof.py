@@ -9,6 +9,7 @@ spread, setup (barriers + TMEM + cluster sync), the predecessor wait (PDL),
 first operands landed, the MMA span, the epilogue tail, and the end.
 usage: gemm_prof.py [--build-only] [MODEL]"""
 import ctypes
+import os
 import subprocess
 import sys
 from pathlib import Path
@@ -52,7 +53,7 @@ buf = np.zeros((CTAS, EV), dtype=np.uint64)
 name = next((a for a in sys.argv[1:] if not a.startswith("-")), "qwen2.5-32b")
 m = MODELS[name].with_layers(1)
 inst = PrefillInstance(m, max_tokens=4096, max_members=32, kv_pages=512)
-inst.capture_graphs(lengths=(256,), depths=(1,))
+inst.capture_graphs(lengths=(16, 256), depths=(1,))
 rng = np.random.default_rng(0)
 qkv_out = (m.n_q_heads + 2 * m.n_kv_heads) * m.head_dim
 proj = {"qkv": (qkv_out, m.hidden), "o": (m.hidden, m.n_q_heads * m.head_dim),
@@ -87,6 +88,11 @@ def scenario(title, l_pad, kind, n_tok):
               flush=True)
 
 
-scenario("512-token chunk (chunk graph)", 512, KIND_STANDARD, 512)
-scenario("256x1 graph bucket, 200 tokens", 256, KIND_GRAPH, 200)
+only = os.environ.get("LP_PROF_ONLY", "")
+if only in ("", "chunk"):
+    scenario("512-token chunk (chunk graph)", 512, KIND_STANDARD, 512)
+if only in ("", "bucket"):
+    scenario("256x1 graph bucket, 200 tokens", 256, KIND_GRAPH, 200)
+if only in ("", "small"):
+    scenario("16x1 graph bucket, 12 tokens", 16, KIND_GRAPH, 12)
 inst.close()
