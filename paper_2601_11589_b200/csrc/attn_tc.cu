@@ -28,6 +28,7 @@
 // scores, bf16 P, fp32 O accumulation; key tiles of 128 instead of 64 change
 // only the online-softmax rescale points.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <stdexcept>
 
@@ -68,6 +69,17 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 __device__ __forceinline__ void st_shared_f32(uint32_t a, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
+__device__ __forceinline__ void st_shared_u16(uint32_t a, uint16_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory");
+}
+__device__ __forceinline__ uint16_t ld_shared_u16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
+// bf16 bits of x rounded toward +inf (-inf stays -inf), and back.
+__device__ __forceinline__ uint16_t bf16_bits_ru(float x) { return __bfloat16_as_ushort(__float2bfloat16_ru(x)); }
+__device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) { return __bfloat162float(__ushort_as_bfloat16(b)); }
 __device__ __forceinline__ float ld_shared_f32(uint32_t a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
@@ -196,7 +208,7 @@ __device__ __forceinline__ float slice_exp_sum(float (&v)[N], float scale, float
 // the first kProfCtas CTAs of KV head 0. Compiled out of the product library.
 #ifdef LP_ATTN_PROF
 constexpr int kProfCtas = 128, kProfSteps = 64;
-__device__ unsigned long long g_attn_prof[kProfCtas][3][kProfSteps][4];
+__device__ unsigned long long g_attn_prof[kProfCtas][3][kProfSteps][8];
 #define ATTN_PROF(role, step, ev)                                                            \
   do {                                                                                       \
     if (blockIdx.y == 0 && blockIdx.x < kProfCtas && (step) < kProfSteps && (step) >= 0)     \
@@ -395,6 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int cc = 0; cc < kHalf / 16; ++cc)
         tmem_ld16(tmem + lane_off + st * kKeys + grp * kHalf + cc * 16, sc + cc * 16);
+      if (prof_me) ATTN_PROF(1, s, 4);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[st]);  // S buffer may be overwritten
@@ -411,6 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       st_shared_f32(rb + (grp * kRows + rt) * 4, mx);
       pair_sync();
       mx = fmaxf(mx, ld_shared_f32(rb + ((grp ^ 1) * kRows + rt) * 4));
+      if (prof_me) ATTN_PROF(1, s, 5);
       const float m_cand = fmaxf(m_run, mx * c.scale_log2);
       // Lazy rescale: keep the reference max unless the row max outgrew it.
       const bool grow = m_cand > m_run + kRescaleTau || (m_run == -INFINITY && m_cand != -INFINITY);
@@ -448,6 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_wait_st();
         }
       }
+      if (prof_me) ATTN_PROF(1, s, 6);
       // P half-row (bf16 pairs) -> TMEM columns [grp*32, grp*32+32) of the P
       // region (the PV MMA reads A from tensor memory: no smem round trip, no
       // async-proxy fence).
@@ -539,12 +554,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 // last-finishing piece from fp32 partials.
 constexpr int kPKStages = 3;
 constexpr int kPVStages = 3;
+// Softmax groups of the persistent kernel (column slices of every step):
+// 4 groups (16 softmax warps, 32 keys each) halve each thread's work per
+// step but measured 2 % slower than 2 (profiles/r02_attn_experiments.md).
+#ifndef LP_ATTN_SOFT_GROUPS
+#define LP_ATTN_SOFT_GROUPS 2
+#endif
+constexpr int kTcpGroups = LP_ATTN_SOFT_GROUPS;
+static_assert(kTcpGroups == 2 || kTcpGroups == 4, "softmax groups: 2 or 4");
+constexpr int kTcpSoftWarps = 4 * kTcpGroups;
+constexpr int kTcpThreads = 64 + 32 * kTcpSoftWarps;
+
 struct TcpSmem {
   static constexpr int kQ = 0;                                  // [32 KiB]
   static constexpr int kK = kQ + kQBytes;                       // [3][32 KiB]
   static constexpr int kV = kK + kPKStages * kQBytes;           // [3][32 KiB]
   static constexpr int kBars = kV + kPVStages * kQBytes;
-  static constexpr int kRed = kBars + 256;                      // float [2 parity][2 group][128 rows]
+  static constexpr int kRed = kBars + 256;  // [2 parity][groups][128 rows]: fp32 for 2 groups, bf16 for 4
   static constexpr int kTotal = kRed + 2 * 2 * kRows * 4;       // 231,680 B of the 232,448 B limit
 };
 
@@ -556,7 +582,7 @@ __device__ __forceinline__ Piece load_piece(const AttnCtx& c, int i) {
   return Piece{a.x, a.y, a.z, a.w, b.x, b.y, b.z};
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kTcpThreads, 1)
     attn_tcp_kernel(const __grid_constant__ CUtensorMap kvm, const AttnCtx c) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -590,11 +616,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], kSoftmaxWarps);
-      mbar_init(&p_ready[i], kSoftmaxWarps);
+      mbar_init(&s_empty[i], kTcpSoftWarps);
+      mbar_init(&p_ready[i], kTcpSoftWarps);
       mbar_init(&p_free[i], 1);
     }
-    mbar_init(q_ready, kSoftmaxWarps);
+    mbar_init(q_ready, kTcpSoftWarps);
     mbar_init(q_free, 1);
     fence_mbar_init();
   }
@@ -696,16 +722,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
+    // kTcpGroups softmax groups of 4 warps; group grp owns key columns
+    // [grp*kSlice, (grp+1)*kSlice) of every step and D columns
+    // [grp*kD/kG, ...) of O. The warps sharing a TMEM lane quarter (one per
+    // group) exchange row maxima through shared memory.
+    constexpr int kG = kTcpGroups;
     const int q4 = warp & 3;
     const int grp = (warp - 2) >> 2;
     const int rt = q4 * 32 + lane;
-    const int stid = threadIdx.x - 64;         // 0..255 among the softmax threads
+    const int stid = threadIdx.x - 64;         // 0..128*kG-1 among the softmax threads
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const uint32_t red = smem_u32(smem + TcpSmem::kRed);
     const int bar_id = 1 + q4;
-    auto pair_sync = [&] { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
-    auto soft_sync = [&] { asm volatile("bar.sync 9, 256;" ::: "memory"); };
-    constexpr int kHalf = kKeys / 2;
+    auto pair_sync = [&] { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(32 * kG) : "memory"); };
+    auto soft_sync = [&] { asm volatile("bar.sync 9, %0;" ::"n"(128 * kG) : "memory"); };
+    constexpr int kHalf = kKeys / kG;          // key columns per group per step
+    constexpr int kDg = kD / kG;               // O columns per group
     int gs = 0;
     for (int i = p_beg, jj = 0; i < p_end; ++i, ++jj) {
       const Piece pc = load_piece(c, i);
@@ -720,7 +752,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (jj >= 1) mbar_wait(q_free, (jj - 1) & 1);
       const __nv_bfloat16* qrow = c.q + (qs + j) * ld_q + hq * kD;
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) cp_async16(tile_addr(q_tile, rt, grp * 8 + ch), qrow + (grp * 8 + ch) * 8);
+      for (int ch = 0; ch < 16 / kG; ++ch)
+        cp_async16(tile_addr(q_tile, rt, grp * (16 / kG) + ch), qrow + (grp * (16 / kG) + ch) * 8);
       asm volatile("cp.async.wait_all;" ::: "memory");
       fence_proxy_async_smem();
       __syncwarp();
@@ -755,10 +788,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (k >= kvalid || kbase + k > pos) sc[k] = -INFINITY;
         }
         float mx = slice_max(sc);
-        const uint32_t rb = red + (x & 1) * 2 * kRows * 4;
-        st_shared_f32(rb + (grp * kRows + rt) * 4, mx);
-        pair_sync();
-        mx = fmaxf(mx, ld_shared_f32(rb + ((grp ^ 1) * kRows + rt) * 4));
+        if constexpr (kG == 2) {
+          const uint32_t rb = red + (x & 1) * 2 * kRows * 4;
+          st_shared_f32(rb + (grp * kRows + rt) * 4, mx);
+          pair_sync();
+          mx = fmaxf(mx, ld_shared_f32(rb + ((grp ^ 1) * kRows + rt) * 4));
+        } else {
+          // bf16 rounded up (the exchange buffer holds 2 parities x kG groups
+          // x 128 rows in 2 KiB): every thread of a row takes the max of the
+          // same kG rounded values, so the reference max stays consistent;
+          // it only has to bound the row (lazy rescale tolerates 2^tau).
+          const uint32_t rb = red + (x & 1) * kG * kRows * 2;
+          st_shared_u16(rb + (grp * kRows + rt) * 2, bf16_bits_ru(mx));
+          pair_sync();
+          mx = -INFINITY;
+#pragma unroll
+          for (int g2 = 0; g2 < kG; ++g2) mx = fmaxf(mx, bf16_bits_to_f32(ld_shared_u16(rb + (g2 * kRows + rt) * 2)));
+        }
         const float m_cand = fmaxf(m_run, mx * c.scale_log2);
         const bool grow = m_cand > m_run + kRescaleTau || (m_run == -INFINITY && m_cand != -INFINITY);
         const float m_new = grow ? m_cand : m_run;
@@ -774,9 +820,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (s > 0 && __any_sync(0xffffffffu, corr != 1.f)) {  // O holds this piece's PVs up to s - 1
           mbar_wait(&p_free[(x - 1) & 1], ((x - 1) >> 1) & 1);
           tc_fence_after();
-          const uint32_t t_o = tmem + lane_off + 2 * kKeys + grp * (kD / 2);
+          const uint32_t t_o = tmem + lane_off + 2 * kKeys + grp * kDg;
 #pragma unroll 1
-          for (int cc = 0; cc < kD / 32; ++cc) {
+          for (int cc = 0; cc < kDg / 16; ++cc) {
             float o[16];
             tmem_ld16(t_o + cc * 16, o);
 #pragma unroll
@@ -786,9 +832,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_wait_st();
         }
         {
-          const uint32_t t_pw = tmem + lane_off + 3 * kKeys + st * 64 + grp * 32;
+          const uint32_t t_pw = tmem + lane_off + 3 * kKeys + st * 64 + grp * (kHalf / 2);
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < kHalf / 32; ++h) {
             float w[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q) w[q] = __uint_as_float(pack_bf16x2(sc[h * 32 + 2 * q], sc[h * 32 + 2 * q + 1]));
@@ -804,21 +850,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Epilogue of the piece: row sum over both column halves, then O / l
       // (bf16) or the fp32 partial of a split unit.
       const int xe = gs + n;  // the next step's exchange parity is free of this piece's max exchange
-      const uint32_t lsum = red + (xe & 1) * 2 * kRows * 4;
-      st_shared_f32(lsum + (grp * kRows + rt) * 4, l_run);
-      pair_sync();
-      const float l_tot = l_run + ld_shared_f32(lsum + ((grp ^ 1) * kRows + rt) * 4);
-      pair_sync();  // the next piece's first step writes this parity again
+      float l_tot;
+      if constexpr (kG == 2) {
+        const uint32_t lsum = red + (xe & 1) * 2 * kRows * 4;
+        st_shared_f32(lsum + (grp * kRows + rt) * 4, l_run);
+        pair_sync();
+        l_tot = l_run + ld_shared_f32(lsum + ((grp ^ 1) * kRows + rt) * 4);
+        pair_sync();  // the next piece's first step writes this parity again
+      } else {
+        // The fp32 row sums need the whole exchange buffer: every softmax
+        // warp is past its last max exchange before it is overwritten, and
+        // every sum is read before the next piece's first exchange.
+        soft_sync();
+        st_shared_f32(red + (grp * kRows + rt) * 4, l_run);
+        pair_sync();
+        l_tot = 0.f;
+#pragma unroll
+        for (int g2 = 0; g2 < kG; ++g2) l_tot += ld_shared_f32(red + (g2 * kRows + rt) * 4);
+        soft_sync();
+      }
       if (n > 0) {
         mbar_wait(&p_free[(xe - 1) & 1], ((xe - 1) >> 1) & 1);
         tc_fence_after();
       }
-      const uint32_t t_o = tmem + lane_off + 2 * kKeys + grp * (kD / 2);
+      const uint32_t t_o = tmem + lane_off + 2 * kKeys + grp * kDg;
       if (pc.ci < 0) {
         const float inv = 1.f / l_tot;
-        __nv_bfloat16* dst = c.out + (qs + j) * ld_q + hq * kD + grp * (kD / 2);
+        __nv_bfloat16* dst = c.out + (qs + j) * ld_q + hq * kD + grp * kDg;
 #pragma unroll 1
-        for (int cc = 0; cc < kD / 32; ++cc) {
+        for (int cc = 0; cc < kDg / 16; ++cc) {
           float o[16];
           tmem_ld16(t_o + cc * 16, o);
           if (pc.row0 + rt < rows_total) {
@@ -832,9 +892,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
       } else {
-        float* dst = c.ws_o + (static_cast<size_t>(pc.slot) * kRows + rt) * kD + grp * (kD / 2);
+        float* dst = c.ws_o + (static_cast<size_t>(pc.slot) * kRows + rt) * kD + grp * kDg;
 #pragma unroll 1
-        for (int cc = 0; cc < kD / 32; ++cc) {
+        for (int cc = 0; cc < kDg / 16; ++cc) {
           float o[16];
           tmem_ld16(t_o + cc * 16, o);
 #pragma unroll
@@ -861,7 +921,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __threadfence();
           const int4 e = c.combine[pc.ci];
           const int first = e.z, np = e.w;
-          for (int it = stid; it < kRows * (kD / 16); it += 256) {
+          for (int it = stid; it < kRows * (kD / 16); it += 128 * kG) {
             const int rl = it / (kD / 16), qc = it % (kD / 16);
             const int mrow = pc.row0 + rl;
             if (mrow >= rows_total) continue;
@@ -912,6 +972,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
 }  // namespace
 
 void attention_prefill_tc(const AttnCtx& c, const CUtensorMap& kv_map, int work_cap, cudaStream_t st) {
@@ -922,8 +983,9 @@ void attention_prefill_tc(const AttnCtx& c, const CUtensorMap& kv_map, int work_
 
 void attention_prefill_tc_persistent(const AttnCtx& c, const CUtensorMap& kv_map, int n_cta, cudaStream_t st) {
   constexpr int smem = TcpSmem::kTotal;
+
   smem_attr_once(reinterpret_cast<const void*>(attn_tcp_kernel), smem);
-  launch_k(attn_tcp_kernel, dim3(n_cta), dim3(kThreads), smem, st, kv_map, c);
+  launch_k(attn_tcp_kernel, dim3(n_cta), dim3(kTcpThreads), smem, st, kv_map, c);
 }
 
 #ifdef LP_ATTN_PROF
@@ -932,7 +994,7 @@ extern "C" int lp_debug_attn_prof(unsigned long long* out, size_t n) {
   return cudaMemcpyFromSymbol(out, g_attn_prof, bytes) == cudaSuccess ? 0 : -1;
 }
 extern "C" int lp_debug_attn_prof_reset() {
-  static unsigned long long zero[kProfCtas][3][kProfSteps][4];
+  static unsigned long long zero[kProfCtas][3][kProfSteps][8];
   return cudaMemcpyToSymbol(g_attn_prof, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
 }
 #endif

@@ -29,7 +29,8 @@ def build_prof():
     obj = PROF / "attn_tc.o"
     src = B.CSRC / "attn_tc.cu"
     subprocess.run([B._nvcc(), *B.ARCH, *B.NVCC_FLAGS, "-DLP_ATTN_PROF", "-c", str(src), "-o", str(obj)], check=True)
-    objs = [o for o in sorted(B.BUILD.glob("*.o")) if o.name != "attn_tc.cu.o"] + [obj]
+    live = [o for o in sorted(B.BUILD.glob("*.o")) if (B.CSRC / o.name[:-2].replace("__", "/")).exists()]
+    objs = [o for o in live if o.name != "attn_tc.cu.o"] + [obj]
     cuda_lib = B._cuda_home() / "lib64"
     subprocess.run([B._nvcc(), *B.ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-L", str(cuda_lib), "-lcudart",
                     "-Xlinker", "-rpath," + str(cuda_lib)], check=True)
@@ -46,7 +47,7 @@ from paper_2601_11589_b200.instance import KIND_STANDARD, QWEN25_7B, Member, Pre
 L = N.lib()
 L.lp_debug_attn_prof.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_size_t]
 CTAS, STEPS = 128, 64
-buf = np.zeros((CTAS, 3, STEPS, 4), dtype=np.uint64)
+buf = np.zeros((CTAS, 3, STEPS, 8), dtype=np.uint64)
 
 m = QWEN25_7B.with_layers(1)
 inst = PrefillInstance(m, max_tokens=4096, max_members=32, kv_pages=1024, use_graphs=False)
@@ -93,6 +94,11 @@ def run(title, members_spec):
             mma_issue=np.median(mma[1:n, 3] - mma[1:n, 2]),
             sm_wait_s=np.median(sm[1:n, 1] - sm[1:n, 0]),
             sm_exp=np.median(sm[1:n, 2] - sm[1:n, 1]),
+            sm_ldtm=np.median(sm[1:n, 4] - sm[1:n, 1]),
+            sm_xchg=np.median(sm[1:n, 5] - sm[1:n, 4]),
+            sm_exps=np.median(sm[1:n, 2] - sm[1:n, 5]),
+            sm_pfree=np.median(sm[1:n, 6] - sm[1:n, 2]),
+            sm_pstore=np.median(sm[1:n, 3] - sm[1:n, 6]),
             sm_tail=np.median(sm[1:n, 3] - sm[1:n, 2]),
             prod_wait=np.median(prod[2:n, 1] - prod[2:n, 0]) if n > 3 else 0,
             first=int(sm[0, 1] - prod[0, 1]) if prod[0, 1] else 0,
