@@ -51,7 +51,7 @@ L.lp_debug_gemm_prof.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_si
 CTAS, EV = 160, 12
 buf = np.zeros((CTAS, EV), dtype=np.uint64)
 name = next((a for a in sys.argv[1:] if not a.startswith("-")), "qwen2.5-32b")
-m = MODELS[name].with_layers(1)
+m = MODELS[name].with_layers(int(os.environ.get("LP_PROF_LAYERS", "1")))
 inst = PrefillInstance(m, max_tokens=4096, max_members=32, kv_pages=512)
 inst.capture_graphs(lengths=(16, 256), depths=(1,))
 rng = np.random.default_rng(0)
