@@ -96,26 +96,6 @@ __device__ __forceinline__ uint32_t tile_addr(uint32_t base, int r, int c) {
   return base + (c >> 3) * kHalfBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4);
 }
 
-// 2^x on the FMA pipe: round-to-nearest split through the 1.5*2^23 magic
-// constant (the integer lands in the low mantissa bits and is shifted into the
-// exponent), degree-5 polynomial on [-0.5, 0.5] (weighted least-squares fit,
-// max relative error 2.4e-7 in fp32 Horner form — the MUFU ex2's level, so the
-// bf16 rounding of P flips no more often than with ex2.approx; the cubic
-// used before (2.1e-4) flipped ~2% of the P values it produced).
-// Inputs are clamped at -126 (-inf -> 2^-126).
-
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;
-  const float f = x - (t - 12582912.f);
-  float p = fmaf(0.0013276408f, f, 0.0096755205f);
-  p = fmaf(p, f, 0.055507131f);
-  p = fmaf(p, f, 0.24022120f);
-  p = fmaf(p, f, 0.69314694f);
-  p = fmaf(p, f, 1.0000001f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
 // Packed fp32x2 arithmetic (FFMA2 / FADD2: two lanes per FMA-pipe issue).
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   float2 d;
@@ -141,7 +121,13 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return d;
 }
 
-// ex2_poly on a pair, packed (same operations per lane, so bit-identical).
+// 2^x for a pair on the FMA pipe (packed fp32x2): round-to-nearest split
+// through the 1.5*2^23 magic constant (the integer lands in the low mantissa
+// bits and is shifted into the exponent), degree-5 polynomial on [-0.5, 0.5]
+// (weighted least-squares fit, max relative error 2.4e-7 in fp32 Horner form —
+// the MUFU ex2's level, so the bf16 rounding of P flips no more often than
+// with ex2.approx; a cubic (2.1e-4) flipped ~2 % of the P values it produced).
+// Inputs are clamped at -126 (-inf -> 2^-126).
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   constexpr float kMagic = 12582912.f;
   x.x = fmaxf(x.x, -126.f);
