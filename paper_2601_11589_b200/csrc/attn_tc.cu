@@ -128,6 +128,9 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 // the MUFU ex2's level, so the bf16 rounding of P flips no more often than
 // with ex2.approx; a cubic (2.1e-4) flipped ~2 % of the P values it produced).
 // Inputs are clamped at -126 (-inf -> 2^-126).
+#ifndef LP_EXP_POLY_DEG
+#define LP_EXP_POLY_DEG 5
+#endif
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   constexpr float kMagic = 12582912.f;
   x.x = fmaxf(x.x, -126.f);
@@ -135,11 +138,22 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   const float2 t = fadd2(x, make_float2(kMagic, kMagic));
   const float2 u = fadd2(t, make_float2(-kMagic, -kMagic));
   const float2 f = ffma2(u, make_float2(-1.f, -1.f), x);
+#if LP_EXP_POLY_DEG == 4  // max relative error 2.6e-6
+  float2 p = ffma2(make_float2(0.009570376f, 0.009570376f), f, make_float2(0.055918723f, 0.055918723f));
+  p = ffma2(p, f, make_float2(0.24024746f, 0.24024746f));
+  p = ffma2(p, f, make_float2(0.69312167f, 0.69312167f));
+  p = ffma2(p, f, make_float2(0.99999928f, 0.99999928f));
+#elif LP_EXP_POLY_DEG == 3  // 7.5e-5
+  float2 p = ffma2(make_float2(0.055174146f, 0.055174146f), f, make_float2(0.24261758f, 0.24261758f));
+  p = ffma2(p, f, make_float2(0.69326109f, 0.69326109f));
+  p = ffma2(p, f, make_float2(0.99992758f, 0.99992758f));
+#else
   float2 p = ffma2(make_float2(0.0013276408f, 0.0013276408f), f, make_float2(0.0096755205f, 0.0096755205f));
   p = ffma2(p, f, make_float2(0.055507131f, 0.055507131f));
   p = ffma2(p, f, make_float2(0.24022120f, 0.24022120f));
   p = ffma2(p, f, make_float2(0.69314694f, 0.69314694f));
   p = ffma2(p, f, make_float2(1.0000001f, 1.0000001f));
+#endif
   return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
