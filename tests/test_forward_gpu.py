@@ -11,11 +11,20 @@ bf16 storage). Page tables bit-exact.
 Greedy first tokens bit-exact wherever the oracle's top-2 margin exceeds 2x
 the max-abs tolerance.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
 
 from oracle import forward_oracle as FO
+
+# Max-abs scale for the 2-layer shape tests when they run under another tile
+# plan (test_two_layer_shapes_under_other_tile_plans): a different split-K /
+# stream-K plan changes the fp32 summation order and so which values round
+# the other way at the bf16 storage points (32B, 2 layers: 0.050 / 0.053
+# max-abs under LP_STREAMK=2 / 0, cosine and mean-abs unchanged).
+TOL_SCALE = float(os.environ.get("LP_PARITY_TOL_SCALE", "1"))
 from oracle.pages import PageOracle
 from paper_2601_11589_b200.instance import (KIND_GRAPH, KIND_PACKED, KIND_STANDARD, TINY, Member,
                                             PrefillInstance, ShapeMismatch)
@@ -114,7 +123,7 @@ def test_7b_shaped_two_layers():
     oracle = FO.OracleModel(FO.with_layers(FO.QWEN25_7B, 2))
     pages = PageOracle(64)
     M = Member
-    tol = (5e-2, 1e-2, 0.9999)
+    tol = (5e-2 * TOL_SCALE, 1e-2, 0.9999)
     _compare(inst, oracle, pages, 256, 2, KIND_GRAPH, [M(0, 0, 200, 0), M(1, 1, 77, 0)], tol=tol)
     _compare(inst, oracle, pages, 128, 1, KIND_GRAPH, [M(2, 0, 100, 200)], tol=tol)
     _compare(inst, oracle, pages, 600, 1, KIND_STANDARD, [M(3, 2, 600, 0)], tol=tol)
@@ -138,7 +147,7 @@ def test_32b_shaped_two_layers():
     oracle = FO.OracleModel(FO.with_layers(FO.QWEN25_32B, 2))
     pages = PageOracle(64)
     M = Member
-    tol = (5e-2, 1e-2, 0.9999)
+    tol = (5e-2 * TOL_SCALE, 1e-2, 0.9999)
     _compare(inst, oracle, pages, 256, 2, KIND_GRAPH, [M(0, 0, 180, 0), M(1, 1, 33, 0)], tol=tol)
     _compare(inst, oracle, pages, 64, 1, KIND_GRAPH, [M(2, 0, 40, 180)], tol=tol)
     _compare(inst, oracle, pages, 512, 1, KIND_STANDARD, [M(3, 2, 512, 0)], tol=tol)
@@ -328,3 +337,22 @@ def test_persistent_attention_split_schedule_32b_shape():
     # history: still <= 4 bf16 ulps, mean 0.0052 measured (0.6 ulp at |v|~1).
     _kv_check(inst, oracle, 3, [0, 1], max_abs=6.25e-2, mean_abs=6e-3)
     inst.close()
+
+
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_two_layer_shapes_under_other_tile_plans(mode):
+    """The 2-layer 7B / 32B parity cases with split-K plans only
+    (LP_STREAMK=0) and with stream-K forced wherever the workspace allows
+    (LP_STREAMK=2: the QKV / O GEMMs too, so qkv_post's per-tile segment
+    table path runs). The planner reads the variable once per process, so
+    each mode runs in a child pytest process."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, LP_STREAMK=mode, LP_PARITY_TOL_SCALE="1.25")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        "tests/test_forward_gpu.py::test_7b_shaped_two_layers",
+                        "tests/test_forward_gpu.py::test_32b_shaped_two_layers"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
