@@ -82,7 +82,7 @@ def committed_traffic(model_name: str, which: int, t_cap: int, n_live: int):
     p = ROOT / "profiles" / "r02_dominant_kernel.json"
     if not p.exists():
         return None
-    for c in json.loads(p.read_text()).get("captures", []):
+    for c in reversed(json.loads(p.read_text()).get("captures", [])):  # the latest capture of that launch
         if (c.get("model"), c.get("which"), c.get("t_cap"), c.get("n_live")) == (model_name, which, t_cap, n_live):
             return c.get("dram_bytes_per_launch")
     return None
