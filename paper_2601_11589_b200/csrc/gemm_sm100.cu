@@ -36,6 +36,10 @@ constexpr int kEpiGroups = LP_GEMM_EPI_GROUPS;
 constexpr int kThreads = 64 + 128 * kEpiGroups;  // warp0 TMA, warp1 MMA, then the epilogue groups
 constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kSmemBudget = 196 * 1024;
+#ifndef LP_GEMM_MAX_STAGES
+#define LP_GEMM_MAX_STAGES 8
+#endif
+constexpr int kMaxStages = LP_GEMM_MAX_STAGES;  // ring depth cap (narrow token tiles fit more)
 // Epilogue staging, double-buffered per epilogue group: SiLU uses [16
 // tokens][64 features] bf16 (both groups), the fused QKV/RoPE epilogue [128
 // rows][17] fp32 (padded: conflict-free; group 0 only).
@@ -48,7 +52,7 @@ struct Cfg {
   static constexpr int kABytes = kBM * kBK * 2;   // 16 KiB
   static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (kSmemBudget / kStageBytes) > 8 ? 8 : (kSmemBudget / kStageBytes);
+  static constexpr int kStages = (kSmemBudget / kStageBytes) > kMaxStages ? kMaxStages : (kSmemBudget / kStageBytes);
   static constexpr int kTmemCols = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int kBarBytes = 256;
   static constexpr int kSmem = 1024 /*align*/ + kStages * kStageBytes + kBarBytes + 2 * kEpiStageBytes +
