@@ -57,6 +57,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
 template <int D>
 __global__ void __launch_bounds__(128)
     attn_prefill_kernel(const __grid_constant__ CUtensorMap kvm, const AttnCtx c) {
+  KTL_SCOPE(kKtlAttnWarp, D);
   constexpr int kChunks = D / 8;           // 16-byte chunks per row
   constexpr int kTileBytes = 64 * D * 2;   // one page of one head
   constexpr int kHalves = D / 64;
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(128)
 // Merge grid: (row blocks that were split, nkv, block_rows / 8), one warp per row.
 template <int D>
 __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnCtx c) {
+  KTL_SCOPE(kKtlAttnCombine, 0);
   pdl_trigger();
   const int ci = blockIdx.x;
   const bool live = ci < *c.n_combine;
@@ -313,3 +315,5 @@ void attention_prefill(const AttnCtx& c, const CUtensorMap& kv_map, int head_dim
 }
 
 }  // namespace lp
+
+KTL_EXPORT(attn)

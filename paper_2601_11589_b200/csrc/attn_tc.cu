@@ -222,6 +222,7 @@ __device__ unsigned long long g_attn_prof[kProfCtas][3][kProfSteps][8];
 
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap kvm, const AttnCtx c) {
+  KTL_SCOPE(kKtlAttnTc, 0);
   // The dynamic window must start 1024-byte aligned (128B-swizzle atoms);
   // trap loudly if it ever does not.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -584,6 +585,7 @@ __device__ __forceinline__ Piece load_piece(const AttnCtx& c, int i) {
 
 __global__ void __launch_bounds__(kTcpThreads, 1)
     attn_tcp_kernel(const __grid_constant__ CUtensorMap kvm, const AttnCtx c) {
+  KTL_SCOPE(kKtlAttnTcp, 0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
@@ -1000,3 +1002,5 @@ extern "C" int lp_debug_attn_prof_reset() {
 #endif
 
 }  // namespace lp
+
+KTL_EXPORT(attn_tc)

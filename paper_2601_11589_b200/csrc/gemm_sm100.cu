@@ -94,6 +94,7 @@ template <int BN, int kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
+  KTL_SCOPE(kKtlGemm, args.M);
   using C = Cfg<BN, kPair>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -690,3 +691,5 @@ void gemm_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs&
 }
 
 }  // namespace lp
+
+KTL_EXPORT(gemm)

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(kRowThreads)
     embed_rmsnorm_kernel(RowCtx c, const int* __restrict__ tokens, const bf16* __restrict__ embed,
                          const bf16* __restrict__ gamma, float* __restrict__ x_resid,
                          bf16* __restrict__ x_norm) {
+  KTL_SCOPE(kKtlEmbed, 0);
   __shared__ float red[33];
   pdl_trigger();
   const int t = blockIdx.x;
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(kRowThreads)
     resid_rmsnorm_kernel(RowCtx c, const float* __restrict__ ws, int splits, const int* splits_dev,
                          const int* __restrict__ sk_tab, size_t ws_stride_rows, float* __restrict__ x_resid,
                          const bf16* __restrict__ gamma, bf16* __restrict__ x_norm) {
+  KTL_SCOPE(kKtlResidNorm, 0);
   __shared__ float red[33];
   pdl_trigger();
   const int t = blockIdx.x;
@@ -182,6 +184,7 @@ __device__ __forceinline__ void st_bf4(bf16* p, float a, float b, float c, float
 }
 template <int U, int SU>
 __global__ void qkv_post_kernel(QkvCtx c) {
+  KTL_SCOPE(kKtlQkvPost, 0);
   __shared__ float s_cos[kQkvMaxHalf], s_sin[kQkvMaxHalf];
   pdl_trigger();
   const int t = blockIdx.x;
@@ -295,6 +298,7 @@ __global__ void qkv_post_kernel(QkvCtx c) {
 // Copies the last-token rows for the LM head and resets the argmax keys.
 __global__ void gather_rows_kernel(const int* n_rows, const int* idx, const bf16* src, bf16* dst, int h,
                                    unsigned long long* keys) {
+  KTL_SCOPE(kKtlGather, 0);
   pdl_trigger();
   const int r = blockIdx.x;
   const bool live = r < *n_rows;
@@ -316,6 +320,7 @@ __device__ __forceinline__ unsigned long long argmax_key(float v, int j) {
 constexpr int kArgmaxChunks = 32;
 __global__ void __launch_bounds__(256)
     argmax_kernel(const int* n_rows, const float* logits, int vocab, unsigned long long* keys) {
+  KTL_SCOPE(kKtlArgmax, 0);
   pdl_trigger();
   const int r = blockIdx.x;
   const bool live = r < *n_rows;
@@ -461,3 +466,5 @@ void argmax_rows(const int* n_rows, int r_cap, const float* logits, int vocab, u
 }
 
 }  // namespace lp
+
+KTL_EXPORT(ops)
