@@ -356,3 +356,30 @@ def test_two_layer_shapes_under_other_tile_plans(mode):
                         "tests/test_forward_gpu.py::test_32b_shaped_two_layers"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_maximum_packed_batch_and_ragged_members():
+    """Capacity edge: a packed batch filling max_tokens (8192 new tokens over
+    16 ragged members, several with resident history) — the largest eager
+    launch (GEMM token tiles and split plans of the full capacity, attention
+    work lists over many members) — and then a single 1-token member, the
+    smallest one. 7B shape, 2 layers, against the oracle."""
+    from paper_2601_11589_b200.instance import QWEN25_7B
+    cfg = QWEN25_7B.with_layers(2)
+    inst = PrefillInstance(cfg, max_tokens=8192, max_members=16, kv_pages=256, use_graphs=False)
+    oracle = FO.OracleModel(FO.with_layers(FO.QWEN25_7B, 2))
+    pages = PageOracle(256)
+    tol = (5e-2 * TOL_SCALE, 1e-2, 0.9999)
+    rng = np.random.default_rng(11)
+    # histories first (4 sessions), then the full batch over 16 sessions
+    hist = [Member(i, 500 + i, int(h), 0) for i, h in enumerate((700, 64, 1, 1300))]
+    _compare(inst, oracle, pages, 0, 0, KIND_PACKED, hist, tol=tol)
+    lens = rng.integers(1, 1024, 16)
+    lens[-1] += 8192 - int(lens.sum()) if lens.sum() < 8192 else 0
+    while lens.sum() > 8192:
+        lens[int(np.argmax(lens))] -= int(lens.sum()) - 8192
+    members = [Member(100 + i, 500 + i, int(n), hist[i].new_tokens if i < 4 else 0) for i, n in enumerate(lens)]
+    assert sum(m.new_tokens for m in members) == 8192
+    _compare(inst, oracle, pages, 0, 0, KIND_PACKED, members, tol=tol)
+    _compare(inst, oracle, pages, 0, 0, KIND_PACKED, [Member(200, 700, 1, 0)], tol=tol)
+    inst.close()
